@@ -1,0 +1,164 @@
+"""Pins for the input generator (STROM relaxation compiler) against the paper.
+
+Printed values: n = 49,500, m = 47,351 and Table 1 block orders
+(PAPER.md:696), 60 localizing blocks; the worked toy rows
+(PAPER.md:344, 361, 382, 409-410); Example 2's basis.
+Invariants: A(X(z)) = b for rollouts, <C, X(z)> = sum f_k(z).
+"""
+from math import comb, sqrt
+
+import numpy as np
+import pytest
+
+from strom_inputs import compile_relaxation, lift_rank1, models, monomial_basis, svec_index
+from strom_inputs.relax import FAMILY_EQ, FAMILY_INEQ, FAMILY_MOM, FAMILY_SEN
+
+
+def _rows(sdp):
+    for i in range(sdp.m):
+        a, b = sdp.A_indptr[i], sdp.A_indptr[i + 1]
+        yield i, dict(zip(sdp.A_indices[a:b].tolist(), sdp.A_data[a:b].tolist()))
+
+
+def test_monomial_basis_example2_and_counts():
+    # Example 2: [z(I_1)]_2 = [1; z2; z3; z2^2; z2 z3; z3^2]
+    B = monomial_basis(2, 2)
+    assert B == [(0, 0), (1, 0), (0, 1), (2, 0), (1, 1), (0, 2)]
+    # s(d, n) = C(n + d, d), against brute-force enumeration
+    import itertools
+    for d in range(1, 6):
+        for n in range(0, 5):
+            brute = [e for e in itertools.product(range(n + 1), repeat=d) if sum(e) <= n]
+            assert len(monomial_basis(d, n)) == len(brute) == comb(n + d, d)
+    assert len(monomial_basis(9, 2)) == 55  # Table 1 pendulum size(M)
+
+
+@pytest.mark.parametrize("N,n,m", [(30, 49500, 47351), (5, 8250, 8476)])
+def test_pendulum_sizes_match_paper(N, n, m):
+    sdp = compile_relaxation(models.pendulum(N, 0.3, 1.0))
+    s = sdp.summary()
+    assert s["n"] == n and s["m"] == m            # PAPER.md:29, 696 (N=30)
+    assert s["moment_blocks"] == N and s["moment_order"] == [55]
+    assert s["localizing_blocks"] == 2 * N and s["localizing_order"] == [10]
+
+
+def test_toy_worked_rows():
+    """The rows printed for the toy problem, clique 2."""
+    dt = 0.1
+    sdp = compile_relaxation(models.toy(N=3, dt=dt), kappa=2)
+    off2 = int(sdp.block_offset[sdp.meta["mom_block"][1]])
+    off3 = int(sdp.block_offset[sdp.meta["mom_block"][2]])
+    offL2 = int(sdp.block_offset[sdp.meta["loc_blocks"][1][0]])
+    M2 = lambda r, c: off2 + svec_index(r - 1, c - 1)   # 1-based as in the paper
+    M3 = lambda r, c: off3 + svec_index(r - 1, c - 1)
+    L2 = lambda r, c: offL2 + svec_index(r - 1, c - 1)
+    rows = list(_rows(sdp))
+    fam = sdp.row_family
+
+    def coef(r, c):
+        return 1.0 if r == c else 1.0 / sqrt(2.0)
+
+    def has_row(target, family):
+        """A row proportional to `target` ({col: matrix-entry coef})."""
+        t = {k: v for k, v in target.items()}
+        for i, row in rows:
+            if fam[i] != family or set(row) != set(t):
+                continue
+            k0 = next(iter(t))
+            lam = row[k0] / t[k0]
+            if all(abs(row[k] - lam * t[k]) < 1e-12 for k in t):
+                return True
+        return False
+
+    # A_mom: M2(2,9) = M2(3,7) = M2(4,6); canonical = (4,6)
+    assert has_row({M2(3, 7): coef(3, 7), M2(4, 6): -coef(4, 6)}, FAMILY_MOM)
+    assert has_row({M2(2, 9): coef(2, 9), M2(4, 6): -coef(4, 6)}, FAMILY_MOM)
+    # A_ineq: L21(1,1) = M2(1,1) - M2(3,3); L21(1,2) = M2(1,2) - M2(3,6) (Q18)
+    assert has_row({L2(1, 1): 1.0, M2(1, 1): -1.0, M2(3, 3): 1.0}, FAMILY_INEQ)
+    assert has_row({L2(1, 2): coef(1, 2), M2(1, 2): -coef(1, 2), M2(3, 6): coef(3, 6)}, FAMILY_INEQ)
+    # A_eq: M2(1,4) + (dt-1) M2(1,2) + dt M2(2,3) = 0
+    assert has_row({M2(1, 4): coef(1, 4), M2(1, 2): (dt - 1) * coef(1, 2),
+                    M2(2, 3): dt * coef(2, 3)}, FAMILY_EQ)
+    # A_sen: M2(1,1)=M3(1,1), M2(1,4)=M3(1,2), M2(4,4)=M3(2,2), M2(4,10)=M3(2,5),
+    # M2(10,10)=M3(5,5)
+    for (a, b_), (c, d) in [((1, 1), (1, 1)), ((1, 4), (1, 2)), ((4, 4), (2, 2)),
+                            ((4, 10), (2, 5)), ((10, 10), (5, 5))]:
+        assert has_row({M2(a, b_): coef(a, b_), M3(c, d): -coef(c, d)}, FAMILY_SEN)
+    # exactly 5 consensus rows between cliques 2 and 3 (s(1, 4) = 5)
+    assert int(np.sum((fam == FAMILY_SEN) & (sdp.row_stage == 1))) == 5
+    # "which leads to 10 linear constraints"
+    assert int(np.sum((fam == FAMILY_EQ) & (sdp.row_stage == 1))) == 10
+
+
+def test_example2_localizing_vector_pattern():
+    """l_phi((z2 - z3) [z(I_1)]_2) rows = phi_{010}-phi_{001}, phi_{020}-phi_{011}, ...
+    (PAPER.md:204-220): the eq rows of a 1-clique POP with h = z2 - z3."""
+    from strom_inputs import Poly
+    from strom_inputs.relax import ChainPop
+    z2, z3 = Poly.var(2, 0), Poly.var(2, 1)
+    pop = ChainPop(d=2, cliques=[[0, 1]], f=[z2 * 0.0 + 1.0], g=[[]], h=[[z2 - z3]], R=[1.0])
+    sdp = compile_relaxation(pop, kappa=2, normalize=False)
+    canon = sdp.meta["canon"][0]
+    inv = {s: mono for mono, s in canon.items()}
+    eq = [row for i, row in _rows(sdp) if sdp.row_family[i] == FAMILY_EQ][:6]
+    expect = [((1, 0), (0, 1)), ((2, 0), (1, 1)), ((1, 1), (0, 2)),
+              ((3, 0), (2, 1)), ((2, 1), (1, 2)), ((1, 2), (0, 3))]
+    for row, (plus, minus) in zip(eq, expect):
+        monos = {inv[c]: v for c, v in row.items()}
+        assert set(monos) == {plus, minus}
+        assert monos[plus] > 0 > monos[minus]
+
+
+def _A(sdp):
+    import scipy.sparse as sp
+    return sp.csr_matrix((sdp.A_data, sdp.A_indices, sdp.A_indptr), shape=(sdp.m, sdp.n))
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_toy_rank1_lift_is_feasible_and_objective(seed):
+    rng = np.random.default_rng(seed)
+    N = 4
+    pop = models.toy(N=N)
+    sdp = compile_relaxation(pop)
+    u = rng.uniform(-1, 1, N)
+    z = models.toy_rollout(N, u)
+    X = lift_rank1(sdp, z)
+    assert np.allclose(_A(sdp) @ X, sdp.b, atol=1e-12)
+    assert abs(sdp.C @ X - pop.objective(z)) < 1e-10           # <C,X(z)> = sum f_k(z)
+
+
+@pytest.mark.parametrize("N", [3, 5])
+def test_pendulum_rank1_lift_is_feasible_and_objective(N):
+    rng = np.random.default_rng(N)
+    th0, thd0 = 0.7, -2.0
+    pop = models.pendulum(N, th0, thd0)
+    sdp = compile_relaxation(pop)
+    u = rng.uniform(-1, 1, N) * 0.3
+    z = models.pendulum_rollout(N, u, th0, thd0)
+    X = lift_rank1(sdp, z)
+    assert np.max(np.abs(_A(sdp) @ X - sdp.b)) < 1e-12
+    assert abs(sdp.C @ X - pop.objective(z)) < 1e-10
+    # a wrong rollout (perturbed control after the fact) violates A(X) = b
+    z2 = z.copy(); z2[4] += 0.1
+    assert np.max(np.abs(_A(sdp) @ lift_rank1(sdp, z2) - sdp.b)) > 1e-4
+
+
+def test_chain_structure_rows_touch_adjacent_stages():
+    sdp = compile_relaxation(models.pendulum(4, 0.2, 0.5))
+    col_block = np.searchsorted(sdp.block_offset, np.arange(sdp.n), side="right") - 1
+    col_stage = sdp.block_stage[col_block]
+    for i, row in _rows(sdp):
+        st = set(col_stage[list(row)].tolist())
+        if sdp.row_family[i] == FAMILY_SEN:
+            assert st == {sdp.row_stage[i], sdp.row_stage[i] + 1}
+        else:
+            assert st == {sdp.row_stage[i]}
+    assert models.pendulum(4).validate_chain() == []
+
+
+def test_synthetic_chain_shapes():
+    sdp = compile_relaxation(models.synthetic_shape("small", 3, seed=0))
+    s = sdp.summary()
+    assert s["moment_order"] == [21] and s["localizing_order"] == [6]
+    pop = models.synthetic_shape("carback", 2, seed=0)
+    assert len(pop.cliques[0]) == 18       # s(18, 2) = 190 (Table 1 car back-in)
