@@ -1,0 +1,193 @@
+/*
+ * strom.h -- C-ABI of the B200-native sGS-ADMM hot path (libstrom.so).
+ *
+ * The library solves the standard multi-block SDP that STROM's sparse moment
+ * relaxation produces (eq:strom:popsdp:standardsdp)
+ *
+ *     min <C, X>  s.t.  A(X) = b,  X = (X_1, ..., X_B) in Omega_+ = prod S^{n_beta}_+
+ *
+ * and its dual  max <b, y>  s.t.  A* y + S = C,  S in Omega_+  
+ * with Algorithm 1 (sGS-ADMM):
+ *
+ *   Step 1  r = b/sigma - A(X/sigma + S - C),  y_half = (eps I + AA*)^{-1} r
+ *   Step 2  X_b = X + sigma (A* y_half - C),   S = (Pi_{Omega+}(X_b) - X_b) / sigma
+ *   Step 3  r = b/sigma - A(X/sigma + S - C),  y = (eps I + AA*)^{-1} r
+ *   Step 4  X = X + tau sigma (S + A* y - C)
+ *
+ * terminating on eta = max(eta_p, eta_d, eta_g) <= tol (eq:strom:sgsadmm:kkt-residual,
+ * PAPER.md:498-510). eps I + AA* is factored once at setup (eq:strom:gpu:cholesky,
+ * PAPER.md:587-591); every per-iteration step runs in hand-written sm_100a
+ * kernels on one device stream.
+ *
+ * Layout conventions
+ *   svec   : SDPT3 symmetric vectorisation: upper triangle,
+ *            column by column, off-diagonal entries multiplied by sqrt(2), so
+ *            <A, B> = svec(A) . svec(B). Block beta occupies svec(n_beta) =
+ *            n_beta (n_beta + 1) / 2 consecutive doubles; blocks are concatenated
+ *            in the order given to strom_sdp_create ("sorted by clique",
+ *            PAPER.md:570). n = sum_beta svec(n_beta).
+ *   rows   : the m constraint rows keep the caller's numbering in every
+ *            host-visible vector (b, y). Internally they are renumbered into
+ *            factor order; that is invisible at this boundary.
+ *   fp64   : all arithmetic and all buffers are IEEE double.
+ *
+ * Ownership: every input is copied at create/setup; the caller may free it on
+ * return. Handles own all device memory. Output buffers are caller-allocated.
+ * Threading: calls on one handle are not thread-safe; distinct handles are
+ * independent. Errors: every call returns a strom_status; strom_last_error()
+ * returns a thread-local message describing the last failure.
+ */
+#ifndef STROM_H
+#define STROM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  STROM_OK = 0,
+  STROM_MAXITER = 1,      /* status, not an error: maxiter reached before tol   */
+  STROM_EINVAL = -1,      /* bad argument / shape / non-chain structure         */
+  STROM_ENOMEM = -2,      /* host or device allocation failed                   */
+  STROM_EFACTOR = -3,     /* non-positive pivot factoring eps I + AA*           */
+  STROM_EEIG = -4,        /* Jacobi eigensolver did not converge                */
+  STROM_EDIVERGED = -5,   /* NaN/Inf in the iterate                             */
+  STROM_ECUDA = -6,       /* CUDA runtime error (message in strom_last_error)   */
+  STROM_ENCCL = -7,       /* NCCL error                                         */
+  STROM_ENOTIMPL = -8     /* feature not built in this version                  */
+} strom_status;
+
+typedef struct strom_sdp strom_sdp;    /* immutable problem data, host side      */
+typedef struct strom_admm strom_admm;  /* solver state bound to device + stream  */
+
+/* One PSD block X_beta of order n. `stage` is its clique
+ * index k (0-based) in the chain (Definition 1); blocks must be
+ * given in non-decreasing stage order and every constraint row may touch blocks
+ * of at most two adjacent stages (the chain-like pattern of Fig. 1 / PAPER.md:415).
+ * A_beta, the columns of A on this block, is CSR over the `nrows` rows that touch
+ * the block: rows[nrows] strictly ascending global row ids in [0, m),
+ * rowptr[nrows + 1] (rowptr[0] = 0), col[] svec index within the block in
+ * [0, svec(n)), val[] the coefficient of svec(A_i). C_svec[svec(n)] is the dense
+ * svec of the objective block C_beta. */
+typedef struct {
+  int32_t n;
+  int32_t stage;
+  int32_t nrows;
+  const int32_t *rows;
+  const int64_t *rowptr;
+  const int32_t *col;
+  const double *val;
+  const double *C_svec;
+} strom_block;
+
+/* Copies and validates the SDP. b[m] is the right-hand side.
+ * EINVAL on: nblocks <= 0, m <= 0, n_beta <= 0, rows not ascending / out of
+ * range, col out of range, stages decreasing, a row touching non-adjacent stages. */
+strom_status strom_sdp_create(strom_sdp **out, int32_t nblocks, const strom_block *blocks,
+                              int32_t m, const double *b);
+void strom_sdp_destroy(strom_sdp *sdp);
+/* n (total svec length) and m of a created SDP. */
+strom_status strom_sdp_dims(const strom_sdp *sdp, int64_t *n, int32_t *m, int32_t *nblocks);
+
+/* Algorithm parameters and the sigma policy (reading Q2). */
+typedef struct {
+  double sigma;          /* sigma > 0 (initial value)                                 */
+  double tau;            /* tau in (0, 2)                                             */
+  double eps_rel;        /* eps = eps_rel * max_i (AA*)_ii when eps <= 0 (reading Q3) */
+  double eps;            /* explicit eps > 0 overrides eps_rel                        */
+  int32_t sigma_period;  /* 0 = fixed sigma; else rebalance every period iterations  */
+  double sigma_ratio;    /* rebalance when eta_d / eta_x leaves [1/ratio, ratio]      */
+  double sigma_factor;   /* multiplicative sigma step                                 */
+  double sigma_min, sigma_max;
+  int32_t check_every;   /* solve(): host polls the device status every K iterations  */
+  int32_t eig_max_sweeps;/* Jacobi sweep cap (reading Q25)                            */
+  double eig_tol;        /* Jacobi stops when off(A) <= eig_tol * ||A||_F             */
+} strom_admm_config;
+
+void strom_admm_default_config(strom_admm_config *cfg);
+
+/* Builds eps I + AA*, orders rows (leaf pairs, stage interiors, separators),
+ * factors once on the host (eq:strom:gpu:cholesky) and uploads everything to
+ * `device`. `cuda_stream` is a cudaStream_t (NULL = the handle creates its own);
+ * e.g. torch.cuda.current_stream().cuda_stream. Multi-GPU horizon partitioning
+ * (nccl_unique_id != NULL, nranks > 1) returns ENOTIMPL in this version.
+ * Starts cold: X = S = 0 (reading Q13). */
+strom_status strom_admm_setup(strom_admm **out, const strom_sdp *sdp, const strom_admm_config *cfg,
+                              int device, void *cuda_stream, const void *nccl_unique_id,
+                              int rank, int nranks);
+void strom_admm_destroy(strom_admm *h);
+
+/* Warm start (Algorithm 1 input X^0, S^0). Host buffers of full
+ * length (X_svec[n], y[m], S_svec[n]); NULL means zeros. Resets the iteration
+ * counter and sigma to cfg.sigma. */
+strom_status strom_admm_set_start(strom_admm *h, const double *X_svec, const double *y,
+                                  const double *S_svec);
+/* Same with device pointers on the handle's device (e.g. torch CUDA tensors). */
+strom_status strom_admm_set_start_device(strom_admm *h, const double *dX, const double *dy,
+                                         const double *dS);
+
+/* Exactly `iters` iterations of Steps 1-4, no tolerance test (eta still
+ * evaluated every iteration). Asynchronous on the handle's stream. */
+strom_status strom_admm_iterate(strom_admm *h, int64_t iters);
+
+/* Iterates until eta <= tol (checked every iteration on the device, polled by
+ * the host every check_every iterations) or maxiter. Returns STROM_OK or
+ * STROM_MAXITER; *iters_done = iterations performed by this call. */
+strom_status strom_admm_solve(strom_admm *h, double tol, int64_t maxiter, int64_t *iters_done);
+
+/* KKT residuals at the current iterate (X^k, y^k, S^k). */
+typedef struct {
+  int64_t iter;
+  double eta_p, eta_d, eta_g;   /* eq:strom:sgsadmm:kkt-residual            */
+  double pobj, dobj;            /* <C, X>, <b, y>                           */
+  double sigma;                 /* sigma that produced this iterate         */
+  double eta_x;                 /* ||X - Pi(X_b)|| / (1 + ||X||), diagnostic */
+} strom_residuals;
+
+/* Copies the iterate to host buffers (NULL = skip). Synchronises the stream. */
+strom_status strom_admm_get(strom_admm *h, double *X_svec, double *y, double *S_svec,
+                            strom_residuals *res);
+/* Device-to-device copy into caller device buffers (NULL = skip). Asynchronous. */
+strom_status strom_admm_get_device(strom_admm *h, double *dX, double *dy, double *dS);
+
+/* Valid lower bound LB = <b,y> + sum_beta R_beta min(0, lambda_min((C - A*y)_beta))
+ * (eq:strom:sgsadmm:valid-lowerbound) at the current y, computed
+ * on the device (A*y and an eigenvalues-only Jacobi). R_beta[nblocks] host array
+ * (Theorem 2). lambda_min[nblocks] optional output. */
+strom_status strom_admm_lower_bound(strom_admm *h, const double *R_beta, double *lb,
+                                    double *lambda_min);
+
+/* Number of kernel launches one iteration issues (for launch accounting). */
+int32_t strom_admm_launches_per_iter(const strom_admm *h);
+/* Size of the factor data on the device in bytes, and unique dense factors. */
+strom_status strom_admm_factor_info(const strom_admm *h, int64_t *device_bytes,
+                                    int32_t *n_leaf_rows, int32_t *n_sep_rows,
+                                    int32_t *n_unique_dense);
+
+strom_status strom_nccl_get_unique_id(void *id128);
+const char *strom_last_error(void);
+const char *strom_version(void);
+
+/* ---- test hooks (not part of the user contract) -----------------------------
+ * Each runs one kernel family on the handle's device on host buffers. */
+/* S_out = (Pi(X_b) - X_b) / sigma per block; also returns Pi(X_b) when non-NULL. */
+strom_status strom_debug_project_psd(strom_admm *h, const double *Xb, double sigma,
+                                     double *S_out, double *Pi_out);
+/* Ax[m] = A(X), Aty[n] = A* y (either may be NULL). */
+strom_status strom_debug_spmv(strom_admm *h, const double *X, double *AX,
+                              const double *y, double *Aty);
+/* y = (eps I + AA*)^{-1} r on the device (rows in caller numbering). */
+strom_status strom_debug_solve(strom_admm *h, const double *r, double *y);
+/* Same solve executed by the HOST from the setup factor (checks the setup
+ * factorisation without a GPU; never used by the iteration). */
+strom_status strom_debug_host_solve(const strom_sdp *sdp, const strom_admm_config *cfg,
+                                    const double *r, double *y);
+/* eps actually used by a handle. */
+double strom_debug_eps(const strom_admm *h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* STROM_H */

@@ -84,27 +84,27 @@ class OracleConfig:
     eps_rel: float = 1e-12        # eps = eps_rel * max diag(AA*) (Q3)
     eps: Optional[float] = None   # explicit eps overrides eps_rel
     sigma_period: int = 0         # 0 => fixed sigma (parity runs)
-    sigma_ratio: float = 5.0
-    sigma_factor: float = 1.5
+    sigma_ratio: float = 2.0
+    sigma_factor: float = 1.2
     sigma_min: float = 1e-4
     sigma_max: float = 1e4
 
 
-def sigma_update(sigma: float, it: int, eta_p: float, eta_d: float, eta_g: float,
+def sigma_update(sigma: float, it: int, eta_d: float, eta_x: float,
                  cfg: OracleConfig) -> float:
     """Residual-balancing sigma policy (reading Q2; PAPER.md:454 only says sigma > 0).
 
-    Every `sigma_period` iterations (it = number of completed iterations):
-    eta_d measures violation of the dual constraint A*y + S = C that sigma
-    penalises, the 'primal side' is max(eta_p, eta_g); if eta_d dominates by more
-    than `sigma_ratio`, sigma *= factor; if the primal side dominates, sigma /= factor.
+    sigma penalises the dual constraint A*y + S = C whose violation is eta_d; the
+    matching ADMM dual residual is eta_x = ||X^{k+1} - Pi(X_b^{k+1})|| / (1 + ||X^{k+1}||),
+    the distance of the multiplier X from the projected point (it scales with sigma).
+    Every `sigma_period` completed iterations: eta_d > ratio * eta_x -> sigma *= factor;
+    eta_x > ratio * eta_d -> sigma /= factor; clamped to [sigma_min, sigma_max].
     """
     if cfg.sigma_period <= 0 or it % cfg.sigma_period != 0:
         return sigma
-    prim = max(eta_p, eta_g)
-    if eta_d > cfg.sigma_ratio * prim:
+    if eta_d > cfg.sigma_ratio * eta_x:
         sigma = min(sigma * cfg.sigma_factor, cfg.sigma_max)
-    elif prim > cfg.sigma_ratio * eta_d:
+    elif eta_x > cfg.sigma_ratio * eta_d:
         sigma = max(sigma / cfg.sigma_factor, cfg.sigma_min)
     return sigma
 
@@ -129,6 +129,7 @@ class Trace:
     pobj: List[float] = field(default_factory=list)
     dobj: List[float] = field(default_factory=list)
     sigma: List[float] = field(default_factory=list)
+    eta_x: List[float] = field(default_factory=list)
 
 
 class Oracle:
@@ -217,13 +218,16 @@ class Oracle:
         self.X, self.S, self.y = X_new, S_new, y_new
         self.it += 1
         ep, ed, eg, po, do = kkt_residuals(self.apply_A(X_new), b, Aty, S_new, C, X_new, y_new)
+        # diagnostic eta_x = ||X^{k+1} - Pi(X_b)|| / (1 + ||X^{k+1}||), Pi(X_b) = X_b + sigma S
+        eta_x = float(np.linalg.norm(X_new - (Xb + sig * S_new)) / (1.0 + np.linalg.norm(X_new)))
         t = self.trace
         t.iters.append(self.it); t.eta_p.append(ep); t.eta_d.append(ed); t.eta_g.append(eg)
         t.pobj.append(po); t.dobj.append(do); t.sigma.append(sig)
-        self.sigma = sigma_update(sig, self.it, ep, ed, eg, self.cfg)
+        t.eta_x.append(eta_x)
+        self.sigma = sigma_update(sig, self.it, ed, eta_x, self.cfg)
         return {"r1": r1, "y_half": y_half, "Xb": Xb, "S": S_new, "r2": r2, "y": y_new,
                 "Aty": Aty, "X": X_new, "eta": (ep, ed, eg), "pobj": po, "dobj": do,
-                "sigma_used": sig}
+                "sigma_used": sig, "eta_x": eta_x}
 
     def iterate(self, iters: int):
         out = None

@@ -1,0 +1,304 @@
+"""Python binding of libstrom (the B200-native sGS-ADMM hot path).
+
+Argument marshalling only: every step of Algorithm 1 runs in
+the sm_100a kernels of `libstrom.so` behind the C-ABI declared in
+`include/strom.h`. Function and method names mirror the C entry points. There is
+no CPU fallback: importing works without a GPU (for build/symbol checks), but
+`strom_admm_setup` fails loudly when no CUDA device or no library is present.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libstrom.so")
+
+STATUS = {0: "STROM_OK", 1: "STROM_MAXITER", -1: "STROM_EINVAL", -2: "STROM_ENOMEM",
+          -3: "STROM_EFACTOR", -4: "STROM_EEIG", -5: "STROM_EDIVERGED", -6: "STROM_ECUDA",
+          -7: "STROM_ENCCL", -8: "STROM_ENOTIMPL"}
+STROM_OK, STROM_MAXITER = 0, 1
+
+# Every symbol include/strom.h declares (checked by tests/test_abi.py).
+EXPORTS = [
+    "strom_sdp_create", "strom_sdp_destroy", "strom_sdp_dims", "strom_admm_default_config",
+    "strom_admm_setup", "strom_admm_destroy", "strom_admm_set_start",
+    "strom_admm_set_start_device", "strom_admm_iterate", "strom_admm_solve", "strom_admm_get",
+    "strom_admm_get_device", "strom_admm_lower_bound", "strom_admm_launches_per_iter",
+    "strom_admm_factor_info", "strom_nccl_get_unique_id", "strom_last_error", "strom_version",
+    "strom_debug_project_psd", "strom_debug_spmv", "strom_debug_solve", "strom_debug_host_solve",
+    "strom_debug_eps",
+]
+
+
+class StromError(RuntimeError):
+    def __init__(self, status: int, where: str, msg: str):
+        super().__init__(f"{where}: {STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class strom_block(C.Structure):
+    _fields_ = [("n", C.c_int32), ("stage", C.c_int32), ("nrows", C.c_int32),
+                ("rows", C.POINTER(C.c_int32)), ("rowptr", C.POINTER(C.c_int64)),
+                ("col", C.POINTER(C.c_int32)), ("val", C.POINTER(C.c_double)),
+                ("C_svec", C.POINTER(C.c_double))]
+
+
+class strom_admm_config(C.Structure):
+    _fields_ = [("sigma", C.c_double), ("tau", C.c_double), ("eps_rel", C.c_double),
+                ("eps", C.c_double), ("sigma_period", C.c_int32), ("sigma_ratio", C.c_double),
+                ("sigma_factor", C.c_double), ("sigma_min", C.c_double), ("sigma_max", C.c_double),
+                ("check_every", C.c_int32), ("eig_max_sweeps", C.c_int32), ("eig_tol", C.c_double)]
+
+
+class strom_residuals(C.Structure):
+    _fields_ = [("iter", C.c_int64), ("eta_p", C.c_double), ("eta_d", C.c_double),
+                ("eta_g", C.c_double), ("pobj", C.c_double), ("dobj", C.c_double),
+                ("sigma", C.c_double), ("eta_x", C.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+_lib: Optional[C.CDLL] = None
+
+
+def load(path: str = LIB_PATH) -> C.CDLL:
+    """Load libstrom.so (raises if it has not been built: no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"libstrom.so not built at {path}; run paper_2406_05846_b200/build.py")
+    lib = C.CDLL(path)
+    P, VP, D, I32, I64 = C.POINTER, C.c_void_p, C.c_double, C.c_int32, C.c_int64
+    sig = {
+        "strom_sdp_create": (I32, [P(VP), I32, P(strom_block), I32, P(D)]),
+        "strom_sdp_destroy": (None, [VP]),
+        "strom_sdp_dims": (I32, [VP, P(I64), P(I32), P(I32)]),
+        "strom_admm_default_config": (None, [P(strom_admm_config)]),
+        "strom_admm_setup": (I32, [P(VP), VP, P(strom_admm_config), C.c_int, VP, VP, C.c_int, C.c_int]),
+        "strom_admm_destroy": (None, [VP]),
+        "strom_admm_set_start": (I32, [VP, P(D), P(D), P(D)]),
+        "strom_admm_set_start_device": (I32, [VP, VP, VP, VP]),
+        "strom_admm_iterate": (I32, [VP, I64]),
+        "strom_admm_solve": (I32, [VP, D, I64, P(I64)]),
+        "strom_admm_get": (I32, [VP, P(D), P(D), P(D), P(strom_residuals)]),
+        "strom_admm_get_device": (I32, [VP, VP, VP, VP]),
+        "strom_admm_lower_bound": (I32, [VP, P(D), P(D), P(D)]),
+        "strom_admm_launches_per_iter": (I32, [VP]),
+        "strom_admm_factor_info": (I32, [VP, P(I64), P(I32), P(I32), P(I32)]),
+        "strom_nccl_get_unique_id": (I32, [VP]),
+        "strom_last_error": (C.c_char_p, []),
+        "strom_version": (C.c_char_p, []),
+        "strom_debug_project_psd": (I32, [VP, P(D), D, P(D), P(D)]),
+        "strom_debug_spmv": (I32, [VP, P(D), P(D), P(D), P(D)]),
+        "strom_debug_solve": (I32, [VP, P(D), P(D)]),
+        "strom_debug_host_solve": (I32, [VP, P(strom_admm_config), P(D), P(D)]),
+        "strom_debug_eps": (D, [VP]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def _check(st: int, where: str):
+    if st not in (STROM_OK, STROM_MAXITER):
+        raise StromError(st, where, load().strom_last_error().decode())
+    return st
+
+
+def _dptr(a: Optional[np.ndarray]):
+    if a is None:
+        return None
+    assert a.dtype == np.float64 and a.flags.c_contiguous
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def strom_admm_default_config(**over) -> strom_admm_config:
+    cfg = strom_admm_config()
+    load().strom_admm_default_config(C.byref(cfg))
+    for k, v in over.items():
+        setattr(cfg, k, v)
+    return cfg
+
+
+class StromSdp:
+    """strom_sdp_create from a BlockSdp-like object (block_n, block_stage,
+    block_offset, A_indptr/A_indices/A_data global CSR, b, C): splits A into the
+    per-block CSR the C-ABI takes."""
+
+    def __init__(self, sdp):
+        lib = load()
+        bn = np.asarray(sdp.block_n, dtype=np.int32)
+        bst = np.asarray(sdp.block_stage, dtype=np.int32)
+        bo = np.asarray(sdp.block_offset, dtype=np.int64)
+        ip = np.asarray(sdp.A_indptr, dtype=np.int64)
+        ind = np.asarray(sdp.A_indices, dtype=np.int64)
+        dat = np.asarray(sdp.A_data, dtype=np.float64)
+        m = int(np.asarray(sdp.b).shape[0])
+        rows_of = np.repeat(np.arange(m, dtype=np.int64), np.diff(ip))
+        blk = np.searchsorted(bo, ind, side="right") - 1
+        order = np.argsort(blk, kind="stable")
+        self._keep = []
+        blocks = (strom_block * len(bn))()
+        starts = np.searchsorted(blk[order], np.arange(len(bn) + 1))
+        Cv = np.ascontiguousarray(np.asarray(sdp.C, dtype=np.float64))
+        for beta in range(len(bn)):
+            sel = order[starts[beta]:starts[beta + 1]]
+            r = rows_of[sel]
+            urows, first, counts = np.unique(r, return_index=True, return_counts=True)
+            rp = np.zeros(len(urows) + 1, dtype=np.int64)
+            rp[1:] = np.cumsum(counts)
+            col = np.ascontiguousarray((ind[sel] - bo[beta]).astype(np.int32))
+            val = np.ascontiguousarray(dat[sel])
+            urows = np.ascontiguousarray(urows.astype(np.int32))
+            cb = np.ascontiguousarray(Cv[bo[beta]:bo[beta + 1]])
+            self._keep += [urows, rp, col, val, cb]
+            blocks[beta] = strom_block(
+                int(bn[beta]), int(bst[beta]), len(urows),
+                urows.ctypes.data_as(C.POINTER(C.c_int32)), rp.ctypes.data_as(C.POINTER(C.c_int64)),
+                col.ctypes.data_as(C.POINTER(C.c_int32)), val.ctypes.data_as(C.POINTER(C.c_double)),
+                cb.ctypes.data_as(C.POINTER(C.c_double)))
+        b = np.ascontiguousarray(np.asarray(sdp.b, dtype=np.float64))
+        h = C.c_void_p()
+        _check(lib.strom_sdp_create(C.byref(h), len(bn), blocks, m, _dptr(b)), "strom_sdp_create")
+        self._keep = None
+        self.handle = h
+        self.m = m
+        self.n = int(bo[-1])
+        self.nblocks = len(bn)
+
+    def dims(self):
+        n, m, nb = C.c_int64(), C.c_int32(), C.c_int32()
+        _check(load().strom_sdp_dims(self.handle, C.byref(n), C.byref(m), C.byref(nb)), "strom_sdp_dims")
+        return n.value, m.value, nb.value
+
+    def host_solve(self, r: np.ndarray, cfg: Optional[strom_admm_config] = None) -> np.ndarray:
+        """strom_debug_host_solve (test hook: host execution of the setup factor)."""
+        cfg = cfg or strom_admm_default_config()
+        r = np.ascontiguousarray(r, dtype=np.float64)
+        y = np.zeros(self.m)
+        _check(load().strom_debug_host_solve(self.handle, C.byref(cfg), _dptr(r), _dptr(y)),
+               "strom_debug_host_solve")
+        return y
+
+    def __del__(self):
+        if getattr(self, "handle", None) and _lib is not None:
+            _lib.strom_sdp_destroy(self.handle)
+            self.handle = None
+
+
+def _torch_stream_ptr(stream):
+    if stream is None:
+        return None
+    return C.c_void_p(int(stream.cuda_stream))
+
+
+class StromAdmm:
+    """strom_admm_setup and friends on one device / stream."""
+
+    def __init__(self, sdp: StromSdp, cfg: Optional[strom_admm_config] = None, device: int = 0,
+                 stream=None):
+        lib = load()
+        self.sdp = sdp
+        self.cfg = cfg or strom_admm_default_config()
+        h = C.c_void_p()
+        _check(lib.strom_admm_setup(C.byref(h), sdp.handle, C.byref(self.cfg), device,
+                                    _torch_stream_ptr(stream), None, 0, 1), "strom_admm_setup")
+        self.handle = h
+        self.n, self.m = sdp.n, sdp.m
+
+    def set_start(self, X=None, y=None, S=None):
+        f = lambda a: None if a is None else np.ascontiguousarray(a, dtype=np.float64)
+        X, y, S = f(X), f(y), f(S)
+        return _check(load().strom_admm_set_start(self.handle, _dptr(X), _dptr(y), _dptr(S)),
+                      "strom_admm_set_start")
+
+    def set_start_device(self, X=None, y=None, S=None):
+        p = lambda t: None if t is None else C.c_void_p(int(t.data_ptr()))
+        return _check(load().strom_admm_set_start_device(self.handle, p(X), p(y), p(S)),
+                      "strom_admm_set_start_device")
+
+    def iterate(self, iters: int):
+        return _check(load().strom_admm_iterate(self.handle, int(iters)), "strom_admm_iterate")
+
+    def solve(self, tol: float, maxiter: int):
+        done = C.c_int64()
+        st = _check(load().strom_admm_solve(self.handle, float(tol), int(maxiter), C.byref(done)),
+                    "strom_admm_solve")
+        return st == STROM_OK, done.value
+
+    def get(self, X=True, y=True, S=True):
+        Xa = np.zeros(self.n) if X else None
+        ya = np.zeros(self.m) if y else None
+        Sa = np.zeros(self.n) if S else None
+        res = strom_residuals()
+        _check(load().strom_admm_get(self.handle, _dptr(Xa), _dptr(ya), _dptr(Sa), C.byref(res)),
+               "strom_admm_get")
+        return Xa, ya, Sa, res.as_dict()
+
+    def get_device(self, X=None, y=None, S=None):
+        p = lambda t: None if t is None else C.c_void_p(int(t.data_ptr()))
+        return _check(load().strom_admm_get_device(self.handle, p(X), p(y), p(S)), "strom_admm_get_device")
+
+    def residuals(self):
+        return self.get(False, False, False)[3]
+
+    def lower_bound(self, R_beta: np.ndarray):
+        R = np.ascontiguousarray(R_beta, dtype=np.float64)
+        lb = C.c_double()
+        lam = np.zeros(self.sdp.nblocks)
+        _check(load().strom_admm_lower_bound(self.handle, _dptr(R), C.byref(lb), _dptr(lam)),
+               "strom_admm_lower_bound")
+        return lb.value, lam
+
+    def launches_per_iter(self) -> int:
+        return int(load().strom_admm_launches_per_iter(self.handle))
+
+    def factor_info(self):
+        b, nl, ns, nu = C.c_int64(), C.c_int32(), C.c_int32(), C.c_int32()
+        _check(load().strom_admm_factor_info(self.handle, C.byref(b), C.byref(nl), C.byref(ns), C.byref(nu)),
+               "strom_admm_factor_info")
+        return {"device_bytes": b.value, "leaf_rows": nl.value, "sep_rows": ns.value, "unique_dense": nu.value}
+
+    def eps(self) -> float:
+        return float(load().strom_debug_eps(self.handle))
+
+    # ---- test hooks ----
+    def debug_project_psd(self, Xb: np.ndarray, sigma: float):
+        Xb = np.ascontiguousarray(Xb, dtype=np.float64)
+        S = np.zeros(self.n); Pi = np.zeros(self.n)
+        _check(load().strom_debug_project_psd(self.handle, _dptr(Xb), float(sigma), _dptr(S), _dptr(Pi)),
+               "strom_debug_project_psd")
+        return S, Pi
+
+    def debug_spmv(self, X: Optional[np.ndarray] = None, y: Optional[np.ndarray] = None):
+        X = None if X is None else np.ascontiguousarray(X, dtype=np.float64)
+        y = None if y is None else np.ascontiguousarray(y, dtype=np.float64)
+        AX = np.zeros(self.m) if X is not None else None
+        Aty = np.zeros(self.n) if y is not None else None
+        _check(load().strom_debug_spmv(self.handle, _dptr(X), _dptr(AX), _dptr(y), _dptr(Aty)),
+               "strom_debug_spmv")
+        return AX, Aty
+
+    def debug_solve(self, r: np.ndarray) -> np.ndarray:
+        r = np.ascontiguousarray(r, dtype=np.float64)
+        y = np.zeros(self.m)
+        _check(load().strom_debug_solve(self.handle, _dptr(r), _dptr(y)), "strom_debug_solve")
+        return y
+
+    def __del__(self):
+        if getattr(self, "handle", None) and _lib is not None:
+            _lib.strom_admm_destroy(self.handle)
+            self.handle = None
+
+
+def strom_version() -> str:
+    return load().strom_version().decode()

@@ -1,0 +1,77 @@
+// Host-side data structures of libstrom (internal; not part of the C-ABI).
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/strom.h"
+
+namespace strom {
+
+void set_error(const std::string &msg);
+
+// Immutable problem data (strom_sdp), assembled into a global row CSR.
+struct Sdp {
+  int32_t nblocks = 0, m = 0, nstages = 0;
+  int64_t n = 0;
+  std::vector<int32_t> bn, bstage;
+  std::vector<int64_t> boff;            // svec offset per block, nblocks + 1
+  std::vector<int64_t> rowptr;          // m + 1
+  std::vector<int32_t> col;             // global svec column
+  std::vector<double> val;
+  std::vector<double> b, C;
+};
+
+// Row-major dense matrix.
+struct Dense {
+  int32_t rows = 0, cols = 0;
+  std::vector<double> a;
+  double *row(int i) { return a.data() + (int64_t)i * cols; }
+  const double *row(int i) const { return a.data() + (int64_t)i * cols; }
+};
+
+// The factorisation of eps I + AA* in "leaf / stage-interior / separator" form
+// (DESIGN.md §K-TRSV). Internal row order: [leaf rows grouped][R_0]...[R_{P-1}][S_0]...[S_{P-2}].
+struct Factor {
+  double eps = 0.0;
+  int32_t m = 0, P = 0;
+  std::vector<int32_t> perm;   // internal -> original row
+  std::vector<int32_t> iperm;  // original -> internal
+  // leaf groups (rows [0, nL))
+  int32_t nL = 0;
+  std::vector<int32_t> gptr;   // ngroups + 1, internal row offsets
+  std::vector<int64_t> goff;   // offsets into gKinv (g*g each)
+  std::vector<double> gKinv;   // K_g^{-1}, row-major g x g
+  // G = K_QL K_LL^{-1}: CSR over Q rows (q - nL), columns = leaf internal index
+  std::vector<int64_t> G_ptr;
+  std::vector<int32_t> G_col;
+  std::vector<double> G_val;
+  // G^T: CSR over leaf rows, columns = absolute internal index of Q rows
+  std::vector<int64_t> Gt_ptr;
+  std::vector<int32_t> Gt_col;
+  std::vector<double> Gt_val;
+  // stage interiors R_k = [R_off[k], R_off[k+1]) ; separators S_j = [S_off[j], S_off[j+1])
+  std::vector<int32_t> R_off;  // P + 1
+  std::vector<int32_t> S_off;  // P (S_0 .. S_{P-2}); S_off[0] = R_off[P]
+  // unique dense stage factors
+  std::vector<Dense> Linv;     // lower-triangular L_k^{-1} (n_k x n_k)
+  std::vector<Dense> F;        // L_k^{-1} K'_{R_k, [S_{k-1} S_k]}  (n_k x (wl + wr))
+  std::vector<int32_t> stage_uid;       // stage -> unique factor id
+  std::vector<int32_t> stage_wl, stage_wr;
+  Dense LTinv;                 // lower-triangular L_T^{-1} (|S| x |S|)
+  int32_t nS() const { return m - (R_off.empty() ? 0 : R_off.back()); }
+};
+
+strom_status build_sdp(Sdp &s, int32_t nblocks, const strom_block *blocks, int32_t m,
+                       const double *b);
+strom_status build_factor(const Sdp &s, double eps_rel, double eps_abs, Factor &f);
+// Host execution of the factored solve (test hook / reference for the device phases).
+void host_solve(const Factor &f, const double *r_orig, double *y_orig);
+
+// dense kernels (dense.cpp)
+bool dense_cholesky_lower(Dense &A);           // in place, lower triangle; false on pivot <= 0
+void dense_trinv_lower(const Dense &L, Dense &X);
+void dense_gemm_lowertri(const Dense &Linv, const Dense &B, Dense &F);  // F = Linv * B
+void dense_sub_AtA(Dense &T, const Dense &F, const std::vector<int32_t> &cmap);  // T[cmap,cmap] -= F^T F
+
+}  // namespace strom

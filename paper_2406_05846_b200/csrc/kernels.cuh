@@ -1,0 +1,51 @@
+// sm_100a kernels of the sGS-ADMM hot path (Algorithm 1).
+// All arithmetic fp64. Every kernel reads sigma/tau from device memory so a
+// captured CUDA graph stays valid when the sigma policy changes sigma, and
+// returns immediately when the device `done` flag is set (solve-to-tol).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace strom {
+
+struct DevState {          // scalars living on the device
+  double sigma, tau, eps;
+  double tol;              // < 0 => never stop (iterate())
+  double normb, normC;
+  int64_t iter;            // completed iterations of this run
+  int32_t done;            // 1 => converged; kernels become no-ops
+  int32_t eig_fail;        // Jacobi exceeded its sweep cap (block id + 1)
+  int32_t nan_flag;
+  int32_t sigma_period;
+  double sigma_ratio, sigma_factor, sigma_min, sigma_max;
+  // residuals of the latest completed iterate
+  double eta_p, eta_d, eta_g, pobj, dobj, eta_x, sigma_used;
+};
+
+// r_i = (b_i - AX_i) / sigma - AS_i + AC_i : Step 1/3 right-hand side
+// (eq:strom:sgsadmm:solve-y1/-y2), formed on the fly by the solve phases.
+struct RhsArgs {
+  const double *b, *ax, *as, *ac;
+};
+
+struct SolveDev {
+  int32_t m, nL, nQ, P, S0, nS;
+  // leaf
+  const int32_t *gptr; int32_t ngroups;
+  const int64_t *goff; const double *gKinv;
+  const int32_t *leaf_group;
+  const int64_t *G_ptr; const int32_t *G_col; const double *G_val;
+  const int64_t *Gt_ptr; const int32_t *Gt_col; const double *Gt_val;
+  // stages
+  const int32_t *R_off, *S_off, *stage_uid, *stage_wl, *stage_wr;
+  // unique dense: Linv (lower, row-major), LinvT (= L^{-T}, row-major upper),
+  // F (n_k x w), Ft (w x n_k)
+  const double *const *Linv; const double *const *LinvT;
+  const double *const *F; const double *const *Ft;
+  const int32_t *uid_n, *uid_w;
+  const double *LTinv, *LTinvT;   // nS x nS
+  // work vectors (internal order, length m)
+  double *u, *v, *t, *z;
+};
+
+}  // namespace strom

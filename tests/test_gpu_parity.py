@@ -1,0 +1,220 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the oracle, element by
+element on the same seeded inputs (SURVEY.md §8(c) parity contract).
+
+Tolerances: single kernels 1e-12 relative (projection),
+1e-13 (SpMV), 1e-10 on range quantities of the solve (A*y; y itself is
+eps-amplified off range(A), F2/Q26); 50 iterations of Algorithm 1: 1e-9
+relative on X, S, A*y and <b, y> (north_star).
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2406_05846_b200 as S                       # noqa: E402
+from oracle import Oracle, OracleConfig, lower_bound, svec_to_mat  # noqa: E402
+from strom_inputs import compile_relaxation, models        # noqa: E402
+from tests import sdp_helpers as H                          # noqa: E402
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / max(1.0, np.linalg.norm(b))
+
+
+_CACHE = {}
+
+
+def case(name):
+    if name not in _CACHE:
+        pop = {"pend5": lambda: models.pendulum(5, 0.3, 1.0),
+               "pend3": lambda: models.pendulum(3, 1.2, -3.0),
+               "pend30": lambda: models.pendulum(30, 0.1, 0.0),
+               "synth": lambda: models.synthetic_shape("small", 6, seed=1),
+               "toy": lambda: models.toy(4)}[name]()
+        _CACHE[name] = compile_relaxation(pop)
+    return _CACHE[name]
+
+
+def make(sdp, **cfg):
+    h = S.StromSdp(sdp)
+    return S.StromAdmm(h, S.strom_admm_default_config(**cfg))
+
+
+# ---------------------------------------------------------------- kernels
+@pytest.mark.parametrize("name", ["pend5", "synth", "toy"])
+def test_projection_parity(name):
+    sdp = case(name)
+    g = make(sdp)
+    o = Oracle(sdp)
+    rng = np.random.default_rng(7)
+    for sigma in (1.0, 0.37):
+        Xb = rng.standard_normal(sdp.n)
+        S_gpu, Pi_gpu = g.debug_project_psd(Xb, sigma)
+        S_ref = (o.project(Xb) - Xb) / sigma
+        bo = sdp.block_offset
+        for beta in range(sdp.nblocks):
+            sl = slice(bo[beta], bo[beta + 1])
+            assert rel(S_gpu[sl], S_ref[sl]) <= 1e-12, (beta, rel(S_gpu[sl], S_ref[sl]))
+
+
+def test_projection_edge_cases():
+    """rank-deficient, PSD, NSD and tiny blocks: Pi is unique even with repeated eigenvalues."""
+    sdp = case("pend5")
+    g = make(sdp)
+    o = Oracle(sdp)
+    rng = np.random.default_rng(8)
+    bo = sdp.block_offset
+    Xb = np.zeros(sdp.n)
+    for beta, nb in enumerate(sdp.block_n):
+        nb = int(nb)
+        kind = beta % 4
+        G = rng.standard_normal((nb, nb))
+        if kind == 0:
+            M = G @ G.T                               # PSD -> S = 0
+        elif kind == 1:
+            M = -G @ G.T                              # NSD -> Pi = 0
+        elif kind == 2:
+            v = rng.standard_normal(nb); M = np.outer(v, v) - 0.5 * np.eye(nb)  # repeated eigs
+        else:
+            M = np.zeros((nb, nb))
+        from oracle import mat_to_svec
+        Xb[bo[beta]:bo[beta + 1]] = mat_to_svec(M)
+    S_gpu, _ = g.debug_project_psd(Xb, 1.0)
+    S_ref = o.project(Xb) - Xb
+    for beta in range(sdp.nblocks):
+        sl = slice(bo[beta], bo[beta + 1])
+        assert np.linalg.norm(S_gpu[sl] - S_ref[sl]) <= 1e-12 * max(1.0, np.linalg.norm(Xb[sl]))
+
+
+@pytest.mark.parametrize("name", ["pend5", "synth", "pend30"])
+def test_spmv_parity(name):
+    sdp = case(name)
+    g = make(sdp)
+    o = Oracle(sdp)
+    rng = np.random.default_rng(9)
+    X = rng.standard_normal(sdp.n); y = rng.standard_normal(sdp.m)
+    AX, Aty = g.debug_spmv(X, y)
+    assert rel(AX, o.apply_A(X)) <= 1e-14
+    assert rel(Aty, o.apply_At(y)) <= 1e-14
+
+
+@pytest.mark.parametrize("name", ["pend5", "synth", "toy", "pend30"])
+def test_solve_parity(name):
+    sdp = case(name)
+    g = make(sdp)
+    o = Oracle(sdp)
+    assert abs(g.eps() - o.eps) <= 1e-15 * o.eps
+    rng = np.random.default_rng(10)
+    for _ in range(2):
+        r = o.apply_A(rng.standard_normal(sdp.n))
+        y = g.debug_solve(r)
+        y2 = o.solve(r)
+        assert np.linalg.norm(o.K @ y - r) <= 1e-11 * np.linalg.norm(r)
+        assert rel(o.apply_At(y), o.apply_At(y2)) <= 1e-10
+
+
+# ---------------------------------------------------------------- iterations
+def _compare(g, o, tol, tag):
+    X, y, Sg, res = g.get()
+    assert rel(X, o.X) <= tol, (tag, "X", rel(X, o.X))
+    assert rel(Sg, o.S) <= tol, (tag, "S", rel(Sg, o.S))
+    assert rel(o.apply_At(y), o.apply_At(o.y)) <= tol, (tag, "A*y")
+    by, by_ref = o.b @ y, o.b @ o.y
+    assert abs(by - by_ref) <= tol * max(1.0, abs(by_ref)), (tag, "<b,y>", by, by_ref)
+    ep, ed, eg, po, do = o.residuals()
+    assert res["iter"] == o.it
+    for a, b, nm in ((res["eta_p"], ep, "eta_p"), (res["eta_d"], ed, "eta_d"), (res["eta_g"], eg, "eta_g")):
+        assert abs(a - b) <= 1e-6 * b + 1e-12, (tag, nm, a, b)
+    assert abs(res["pobj"] - po) <= tol * max(1.0, abs(po))
+    return res
+
+
+@pytest.mark.parametrize("name,sigma,tau", [("pend5", 1.0, 1.618), ("synth", 0.5, 1.95),
+                                            ("toy", 2.0, 1.0), ("pend3", 1.0, 1.618)])
+def test_50_iterations_parity(name, sigma, tau):
+    sdp = case(name)
+    g = make(sdp, sigma=sigma, tau=tau, check_every=10)
+    o = Oracle(sdp, OracleConfig(sigma=sigma, tau=tau))
+    done = 0
+    for target in (1, 10, 50):
+        g.iterate(target - done)
+        o.iterate(target - done)
+        done = target
+        _compare(g, o, 1e-9, f"{name}@{target}")
+
+
+def test_full_size_pendulum30_parity():
+    """BASELINE configs[1] (n = 49,500, m = 47,351) in the bench's launch configuration."""
+    sdp = case("pend30")
+    g = make(sdp, check_every=50)
+    o = Oracle(sdp)
+    g.iterate(5); o.iterate(5)
+    _compare(g, o, 1e-9, "pend30@5")
+    g.iterate(45); o.iterate(45)
+    _compare(g, o, 1e-9, "pend30@50")
+
+
+def test_warm_start_parity():
+    sdp = case("pend5")
+    o = Oracle(sdp)
+    o.iterate(30)
+    g = make(sdp)
+    g.set_start(o.X, o.y, o.S)
+    o2 = Oracle(sdp)
+    o2.set_start(o.X, o.y, o.S)
+    g.iterate(20); o2.iterate(20)
+    _compare(g, o2, 1e-9, "warm")
+
+
+def test_adaptive_sigma_parity():
+    """The sigma policy (reading Q2) runs on the device; same rule in the oracle."""
+    sdp = case("pend5")
+    kw = dict(sigma=1.0, sigma_period=5, sigma_ratio=2.0, sigma_factor=1.2)
+    g = make(sdp, **kw)
+    o = Oracle(sdp, OracleConfig(**kw))
+    g.iterate(40); o.iterate(40)
+    res = _compare(g, o, 1e-8, "adaptive")
+    assert abs(res["sigma"] - o.trace.sigma[-1]) <= 1e-12
+
+
+@pytest.mark.parametrize("case_name", ["one", "simplex", "lovasz", "chain"])
+def test_closed_form_solve(case_name):
+    sdp, opt = {"one": H.one_by_one, "simplex": H.trace_simplex,
+                "lovasz": H.lovasz_c5, "chain": H.two_stage_chain}[case_name]()
+    g = make(sdp, eps_rel=1e-14, check_every=20)
+    ok, it = g.solve(1e-9, 20000)
+    assert ok, (case_name, it, g.residuals())
+    res = g.residuals()
+    assert abs(res["pobj"] - opt) <= 1e-7 * (1 + abs(opt))
+    assert abs(res["dobj"] - opt) <= 1e-7 * (1 + abs(opt))
+
+
+def test_solve_to_tol_pendulum5_certified():
+    """Solve to eta <= 1e-6 on the GPU, then the oracle's certificate on the GPU's y."""
+    from oracle import extract_pendulum, suboptimality_gap
+    sdp = case("pend5")
+    g = make(sdp, check_every=25)
+    ok, it = g.solve(1e-6, 20000)
+    assert ok
+    X, y, Sg, res = g.get()
+    assert max(res["eta_p"], res["eta_d"], res["eta_g"]) <= 1e-6
+    o = Oracle(sdp)
+    LB, lam = lower_bound(sdp, y, o.apply_At(y), safety=False)
+    LBg, lamg = g.lower_bound(sdp.R_beta)
+    assert abs(LBg - LB) <= 1e-9 * max(1, abs(LB))
+    assert np.max(np.abs(lamg - lam)) <= 1e-10
+    z, p_hat, feas = extract_pendulum(sdp, X)
+    xi = suboptimality_gap(p_hat, LBg)
+    assert feas and xi < 1e-2
+
+
+def test_single_stage_no_separators():
+    sdp, _ = H.trace_simplex(seed=3, sizes=(5, 1, 6, 2))
+    g = make(sdp)
+    o = Oracle(sdp)
+    g.iterate(20); o.iterate(20)
+    _compare(g, o, 1e-9, "single-stage")
