@@ -166,6 +166,13 @@ strom_status strom_admm_factor_info(const strom_admm *h, int64_t *device_bytes,
                                     int32_t *n_leaf_rows, int32_t *n_sep_rows,
                                     int32_t *n_unique_dense);
 
+/* Per-kernel device times (ms) of the instrumented iteration: the last iteration
+ * of the most recent check_every-iteration graph launch carries CUDA event
+ * record nodes around each of its kernel launches (on the handle's stream).
+ * Fills ms[i] and names[i] (static strings) for i < min(count, cap); returns the
+ * number of launches per iteration, or a negative strom_status. */
+int32_t strom_admm_kernel_times(strom_admm *h, double *ms, const char **names, int32_t cap);
+
 strom_status strom_nccl_get_unique_id(void *id128);
 const char *strom_last_error(void);
 const char *strom_version(void);

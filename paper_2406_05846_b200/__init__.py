@@ -28,7 +28,7 @@ EXPORTS = [
     "strom_admm_setup", "strom_admm_destroy", "strom_admm_set_start",
     "strom_admm_set_start_device", "strom_admm_iterate", "strom_admm_solve", "strom_admm_get",
     "strom_admm_get_device", "strom_admm_lower_bound", "strom_admm_launches_per_iter",
-    "strom_admm_factor_info", "strom_nccl_get_unique_id", "strom_last_error", "strom_version",
+    "strom_admm_factor_info", "strom_admm_kernel_times", "strom_nccl_get_unique_id", "strom_last_error", "strom_version",
     "strom_debug_project_psd", "strom_debug_spmv", "strom_debug_solve", "strom_debug_host_solve",
     "strom_debug_eps",
 ]
@@ -91,6 +91,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "strom_admm_lower_bound": (I32, [VP, P(D), P(D), P(D)]),
         "strom_admm_launches_per_iter": (I32, [VP]),
         "strom_admm_factor_info": (I32, [VP, P(I64), P(I32), P(I32), P(I32)]),
+        "strom_admm_kernel_times": (I32, [VP, P(D), P(C.c_char_p), I32]),
         "strom_nccl_get_unique_id": (I32, [VP]),
         "strom_last_error": (C.c_char_p, []),
         "strom_version": (C.c_char_p, []),
@@ -196,9 +197,15 @@ class StromSdp:
 
 
 def _torch_stream_ptr(stream):
+    """cudaStream_t of a torch stream. torch's legacy default stream has handle 0,
+    which the C-ABI would read as "create your own stream"; refuse it so that
+    events recorded by the caller always see the solver's work."""
     if stream is None:
         return None
-    return C.c_void_p(int(stream.cuda_stream))
+    ptr = int(stream.cuda_stream)
+    if ptr == 0:
+        raise ValueError("pass a non-default torch.cuda.Stream() (the legacy default stream is 0)")
+    return C.c_void_p(ptr)
 
 
 class StromAdmm:
@@ -258,6 +265,16 @@ class StromAdmm:
         _check(load().strom_admm_lower_bound(self.handle, _dptr(R), C.byref(lb), _dptr(lam)),
                "strom_admm_lower_bound")
         return lb.value, lam
+
+    def kernel_times(self):
+        """[(kernel name, ms)] of the instrumented iteration of the last graph launch."""
+        cap = 256
+        ms = np.zeros(cap)
+        names = (C.c_char_p * cap)()
+        cnt = load().strom_admm_kernel_times(self.handle, _dptr(ms), names, cap)
+        if cnt < 0:
+            _check(cnt, "strom_admm_kernel_times")
+        return [(names[i].decode(), float(ms[i])) for i in range(min(cnt, cap))]
 
     def launches_per_iter(self) -> int:
         return int(load().strom_admm_launches_per_iter(self.handle))

@@ -544,7 +544,13 @@ struct strom_admm {
   int K = 50;
   int launches_per_iter = 0;
   double *lam_dev = nullptr;
+  // per-kernel event instrumentation of one iteration inside the K-graph
+  std::vector<cudaEvent_t> prof_ev;
+  std::vector<const char *> prof_names;
+  bool prof_capture = false;
+  int prof_idx = 0, prof_count = 0;
   ~strom_admm() {
+    for (cudaEvent_t e : prof_ev) cudaEventDestroy(e);
     if (execK) cudaGraphExecDestroy(execK);
     if (exec1) cudaGraphExecDestroy(exec1);
     if (graphK) cudaGraphDestroy(graphK);
@@ -573,34 +579,51 @@ struct strom_admm {
 
 namespace {
 
+constexpr int kMaxProfEvents = 96;
+
+// Records an external event node in front of the next kernel while the
+// instrumented iteration is being captured (name == nullptr closes the list).
+void mark(strom_admm *h, const char *name) {
+  if (!h->prof_capture || h->prof_idx >= (int)h->prof_ev.size()) return;
+  cudaEventRecordWithFlags(h->prof_ev[h->prof_idx], h->stream, cudaEventRecordExternal);
+  h->prof_names[h->prof_idx] = name;
+  ++h->prof_idx;
+}
+
 strom_status launch_solve(strom_admm *h, const RhsArgs &ra, double *y, int &nl) {
   const SolveDev &d = h->sd;
   cudaStream_t s = h->stream;
   const int TB = 256;
   nl = 0;
-  if (d.nQ > 0) { k_solve_p1<<<(d.nQ + TB - 1) / TB, TB, 0, s>>>(d, ra, h->st); ++nl; }
+  if (d.nQ > 0) { mark(h, "trsv_p1_leaf_fwd"); k_solve_p1<<<(d.nQ + TB - 1) / TB, TB, 0, s>>>(d, ra, h->st); ++nl; }
   if (h->nitems > 0) {
+    mark(h, "trsv_p2_stage_Linv");
     k_gemv_stage<<<(h->nitems * 32 + TB - 1) / TB, TB, 0, s>>>(d, h->items, h->nitems, h->stage_list, 0,
                                                                d.u, d.v, h->st);
     ++nl;
   }
   if (d.nS > 0) {
+    mark(h, "trsv_p3_sep_rhs");
     k_solve_p3<<<(d.nS * 32 + TB - 1) / TB, TB, 0, s>>>(d, h->st); ++nl;
+    mark(h, "trsv_p4_sep_LTinv");
     k_solve_sep<<<(d.nS * 32 + TB - 1) / TB, TB, 0, s>>>(d, 0, y, h->st); ++nl;
+    mark(h, "trsv_p5_sep_LTinvT");
     k_solve_sep<<<(d.nS * 32 + TB - 1) / TB, TB, 0, s>>>(d, 1, y, h->st); ++nl;
   }
   const int nR = d.S0 - d.nL;
   if (nR > 0) {
     if (d.nS > 0) {
+      mark(h, "trsv_p6a_stage_F");
       k_solve_p6a<<<(nR * 32 + TB - 1) / TB, TB, 0, s>>>(d, h->row_stage_R, y, h->st); ++nl;
     } else {
       CK(cudaMemcpyAsync(d.t + d.nL, d.v + d.nL, sizeof(double) * nR, cudaMemcpyDeviceToDevice, s));
     }
+    mark(h, "trsv_p6b_stage_LinvT");
     k_gemv_stage<<<(h->nitems * 32 + TB - 1) / TB, TB, 0, s>>>(d, h->items, h->nitems, h->stage_list, 1,
                                                                d.t, y, h->st);
     ++nl;
   }
-  if (d.nL > 0) { k_solve_p7<<<(d.nL + TB - 1) / TB, TB, 0, s>>>(d, ra, y, h->st); ++nl; }
+  if (d.nL > 0) { mark(h, "trsv_p7_leaf_bwd"); k_solve_p7<<<(d.nL + TB - 1) / TB, TB, 0, s>>>(d, ra, y, h->st); ++nl; }
   CK(cudaGetLastError());
   return STROM_OK;
 }
@@ -623,6 +646,9 @@ strom_status launch_eig(strom_admm *h, int mode, const double *yv, int &nl) {
     a.mode = mode; a.lam_min = h->lam_dev;
     const int threads = np <= 16 ? 64 : (np <= 64 ? 256 : 512);
     const size_t smem = eig_smem(np, np);
+    static const char *eig_names[] = {"eig_class0", "eig_class1", "eig_class2", "eig_class3",
+                                      "eig_class4", "eig_class5", "eig_class6", "eig_class7"};
+    mark(h, eig_names[c < 8 ? c : 7]);
     k_eig<<<a.nblk, threads, smem, h->stream>>>(a);
     ++nl;
   }
@@ -644,14 +670,19 @@ strom_status launch_iteration(strom_admm *h, int &nl_total) {
   if ((st = launch_eig(h, 0, h->yh, nl)) != STROM_OK) return st;
   nl_total += nl;
   // Step 3: A S^{k+1}, then solve
+  mark(h, "spmv_AS");
   k_spmv<<<(h->m + TB - 1) / TB, TB, 0, s>>>(h->m, h->Arp, h->Aci, h->Av, h->S, h->AS, h->st);
   nl_total += 1;
   if ((st = launch_solve(h, ra, h->y, nl)) != STROM_OK) return st;
   nl_total += nl;
   // Step 4 + residual partials
+  mark(h, "update_X");
   k_update<<<h->nup, TB, 0, s>>>(h->n, h->Atp, h->Atr, h->Atv, h->y, h->X, h->S, h->C, h->Xb, h->part_up, h->st);
+  mark(h, "spmv_AX_resid");
   k_spmv_ax<<<h->nax, TB, 0, s>>>(h->m, h->Arp, h->Aci, h->Av, h->X, h->AX, h->b, h->y, h->part_ax, h->st);
+  mark(h, "finalize");
   k_finalize<<<1, kRedThreads, 0, s>>>(h->part_ax, h->nax, h->part_up, h->nup, h->st);
+  mark(h, nullptr);
   nl_total += 3;
   CK(cudaGetLastError());
   return STROM_OK;
@@ -662,7 +693,12 @@ strom_status capture(strom_admm *h, int iters, cudaGraph_t &g, cudaGraphExec_t &
   strom_status st = STROM_OK;
   for (int i = 0; i < iters && st == STROM_OK; ++i) {
     int nl = 0;
+    const bool instrument = (iters == h->K && i == iters - 1 && !h->prof_ev.empty());
+    h->prof_capture = instrument;
+    h->prof_idx = 0;
     st = launch_iteration(h, nl);
+    if (instrument) h->prof_count = h->prof_idx;
+    h->prof_capture = false;
     h->launches_per_iter = nl;
   }
   cudaGraph_t graph = nullptr;
@@ -903,6 +939,9 @@ strom_status strom_admm_setup(strom_admm **out, const strom_sdp *sdp_h, const st
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(h->stream));
   // ---- graphs ---------------------------------------------------------------
+  h->prof_ev.resize(kMaxProfEvents);
+  h->prof_names.assign(kMaxProfEvents, nullptr);
+  for (auto &e : h->prof_ev) CK(cudaEventCreate(&e));
   if ((st = capture(h.get(), h->K, h->graphK, h->execK))) return st;
   if ((st = capture(h.get(), 1, h->graph1, h->exec1))) return st;
   *out = h.release();
@@ -1043,6 +1082,20 @@ strom_status strom_admm_lower_bound(strom_admm *h, const double *R_beta, double 
 }
 
 int32_t strom_admm_launches_per_iter(const strom_admm *h) { return h ? h->launches_per_iter : 0; }
+
+int32_t strom_admm_kernel_times(strom_admm *h, double *ms, const char **names, int32_t cap) {
+  if (!h) { set_error("strom_admm_kernel_times: NULL handle"); return STROM_EINVAL; }
+  if (cudaStreamSynchronize(h->stream) != cudaSuccess) { set_error("stream sync failed"); return STROM_ECUDA; }
+  const int cnt = std::max(0, h->prof_count - 1);
+  for (int i = 0; i < cnt && i < cap; ++i) {
+    float t = 0.f;
+    cudaError_t e = cudaEventElapsedTime(&t, h->prof_ev[i], h->prof_ev[i + 1]);
+    if (ms) ms[i] = (e == cudaSuccess) ? (double)t : -1.0;
+    if (names) names[i] = h->prof_names[i];
+  }
+  cudaGetLastError();
+  return cnt;
+}
 
 strom_status strom_admm_factor_info(const strom_admm *h, int64_t *device_bytes, int32_t *n_leaf_rows,
                                     int32_t *n_sep_rows, int32_t *n_unique_dense) {

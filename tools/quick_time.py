@@ -9,7 +9,7 @@ for N in (5, 30):
     t0 = time.time()
     sdp = compile_relaxation(models.pendulum(N, 0.1, 0.0))
     t1 = time.time()
-    g = S.StromAdmm(S.StromSdp(sdp), S.strom_admm_default_config(check_every=50), stream=torch.cuda.current_stream())
+    st = torch.cuda.Stream(); g = S.StromAdmm(S.StromSdp(sdp), S.strom_admm_default_config(check_every=50), stream=st); torch.cuda.set_stream(st)
     t2 = time.time()
     print(f"N={N} gen {t1-t0:.2f}s setup {t2-t1:.2f}s", g.factor_info(), "launches/iter", g.launches_per_iter(), flush=True)
     g.iterate(100); torch.cuda.synchronize()
