@@ -103,7 +103,9 @@ typedef struct {
   double sigma_min, sigma_max;
   int32_t check_every;   /* solve(): host polls the device status every K iterations  */
   int32_t eig_max_sweeps;/* Jacobi sweep cap (reading Q25)                            */
-  double eig_tol;        /* Jacobi stops when off(A) <= eig_tol * ||A||_F             */
+  double eig_tol;        /* Jacobi rotates a column pair while |cos| > max(eig_tol, 4nu) */
+  int32_t eig_warm;      /* 1 = start Jacobi from the previous iteration's eigenbasis */
+  int32_t eig_cold_every;/* > 0: cold Jacobi start every this many iterations        */
 } strom_admm_config;
 
 void strom_admm_default_config(strom_admm_config *cfg);
@@ -144,6 +146,7 @@ typedef struct {
   double pobj, dobj;            /* <C, X>, <b, y>                           */
   double sigma;                 /* sigma that produced this iterate         */
   double eta_x;                 /* ||X - Pi(X_b)|| / (1 + ||X||), diagnostic */
+  int64_t eig_sweeps;           /* Jacobi sweeps summed over blocks since setup */
 } strom_residuals;
 
 /* Copies the iterate to host buffers (NULL = skip). Synchronises the stream. */

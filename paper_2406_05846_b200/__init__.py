@@ -51,13 +51,14 @@ class strom_admm_config(C.Structure):
     _fields_ = [("sigma", C.c_double), ("tau", C.c_double), ("eps_rel", C.c_double),
                 ("eps", C.c_double), ("sigma_period", C.c_int32), ("sigma_ratio", C.c_double),
                 ("sigma_factor", C.c_double), ("sigma_min", C.c_double), ("sigma_max", C.c_double),
-                ("check_every", C.c_int32), ("eig_max_sweeps", C.c_int32), ("eig_tol", C.c_double)]
+                ("check_every", C.c_int32), ("eig_max_sweeps", C.c_int32), ("eig_tol", C.c_double),
+                ("eig_warm", C.c_int32), ("eig_cold_every", C.c_int32)]
 
 
 class strom_residuals(C.Structure):
     _fields_ = [("iter", C.c_int64), ("eta_p", C.c_double), ("eta_d", C.c_double),
                 ("eta_g", C.c_double), ("pobj", C.c_double), ("dobj", C.c_double),
-                ("sigma", C.c_double), ("eta_x", C.c_double)]
+                ("sigma", C.c_double), ("eta_x", C.c_double), ("eig_sweeps", C.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

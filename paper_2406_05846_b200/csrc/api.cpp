@@ -73,6 +73,8 @@ void strom_admm_default_config(strom_admm_config *cfg) {
   cfg->check_every = 50;
   cfg->eig_max_sweeps = 40;
   cfg->eig_tol = 1e-15;
+  cfg->eig_warm = 1;
+  cfg->eig_cold_every = 0;
 }
 
 }  // extern "C"

@@ -1,0 +1,279 @@
+// K-EIG: batched PSD-cone projection (Step 2 of Algorithm 1, PAPER.md:467-472;
+// projection Pi(X) = Q max(0, W) Q^T), included by engine.cu.
+//
+// One CTA per PSD block X_beta (order n <= 118), fp64 throughout:
+//   1. gather X_b = X + sigma (A* y - C) straight from svec (A* fused);
+//   2. one-sided (Hestenes) Jacobi on the shifted matrix B = X_b + s I, s = ||X_b||_F,
+//      so that B is PSD with eigenvalues lambda + s >= 0 kept apart even when X_b has
+//      +/- pairs: U = B V, columns of U rotated pairwise until mutually orthogonal,
+//      then u_j = (lambda_j + s) v_j. One warp owns one column pair per round
+//      (round-robin ordering), so a round needs a single CTA barrier;
+//   3. warm start: V is the eigenbasis of the previous ADMM iteration (stored per
+//      block), so near convergence one sweep plus one checking sweep suffice;
+//   4. S = (Pi(X_b) - X_b)/sigma from the smaller of the positive and negative
+//      eigen-sets (Moreau: Pi(X) - X = Pi(-X)), written back in svec.
+#pragma once
+
+struct EigArgs {
+  const int32_t *blocks; int32_t nblk;
+  const int32_t *bn; const int64_t *boff;
+  const int64_t *Atp; const int32_t *Atr; const double *Atv;
+  const double *X, *C, *y;
+  double *Xb_out, *S_out;
+  double *Vstore; const int64_t *voff;     // warm-start eigenbases (n*n per block)
+  DevState *st;
+  int32_t max_sweeps; double tol;
+  int32_t mode;          // 0 projection; 1 eigenvalues of C - A*y (lambda_min only)
+  int32_t warm_enable, cold_every;
+  double *lam_min;
+};
+
+__device__ __forceinline__ int rr_pos(int j, int r, int NPm1) {
+  // round-robin position (circle method): player 0 fixed, others rotate by r
+  if (j == 0) return 0;
+  int t = j - 1 + r;
+  if (t >= NPm1) t -= NPm1;
+  return 1 + t;
+}
+
+__device__ __forceinline__ int svec_pos(int i, int j) {  // i, j any order
+  return (i <= j) ? (j * (j + 1) / 2 + i) : (i * (i + 1) / 2 + j);
+}
+
+// G lanes own one column pair (rows i = sub + G*c), 32/G pairs per warp.
+template <int G, int EPL>
+__global__ void __launch_bounds__(512, 1) k_eig(EigArgs a) {
+  if (a.st->done) return;
+  extern __shared__ double sm[];
+  __shared__ double red[4 * 32];
+  __shared__ int sets[128];
+  __shared__ int set_info;
+  constexpr int PPW = 32 / G;
+  const int bidx = a.blocks[blockIdx.x];
+  const int n = a.bn[bidx];
+  const int NP = n + (n & 1), H = NP / 2;
+  const int64_t off = a.boff[bidx];
+  const int L = n * (n + 1) / 2;
+  double *U = sm;                 // n columns x n rows, column-major (column j at U + j*n)
+  double *V = sm + n * n;         // same layout
+  double *lamv = sm + 2 * n * n;  // n eigenvalues
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5, nwarps = nt >> 5;
+  const int grp = lane / G, sub = lane % G;
+  const double sigma = a.st->sigma;
+  const double isq2 = 0.70710678118654752440;
+  const bool proj = (a.mode == 0);
+  const bool warm = proj && a.warm_enable && a.st->eig_warm_valid && n * n <= 16 * nt &&
+                    (a.cold_every <= 0 || (a.st->iter % a.cold_every) != 0);
+  // ---- 1. gather X_b (svec) into global, Frobenius norm -------------------------
+  double fro = 0.0;
+  for (int e = tid; e < L; e += nt) {
+    const int64_t J = off + e;
+    double aty = 0.0;
+    for (int64_t t = a.Atp[J]; t < a.Atp[J + 1]; ++t) aty += a.Atv[t] * a.y[a.Atr[t]];
+    const double xb = proj ? a.X[J] + sigma * (aty - a.C[J]) : a.C[J] - aty;
+    a.Xb_out[J] = xb;              // mode 1 uses Xb_out as scratch for C - A*y
+    fro += xb * xb;                // svec norm == Frobenius norm
+  }
+  {
+    double v1[1] = {fro};
+    block_sum<1>(v1, red);
+    if (tid == 0) red[127] = sqrt(v1[0]);
+    __syncthreads();
+  }
+  const double s = red[127] * (1.0 + 1e-12) + 1e-300;   // s >= ||X_b||_2
+  const double *Xb = a.Xb_out + off;
+  // ---- 2. U = (X_b + s I) V with V = V_prev (warm) or I ----------------------------
+  for (int e = tid; e < n * n; e += nt) {   // A (symmetric) into U
+    const int j = e / n, i = e - j * n;
+    const double v = Xb[svec_pos(i, j)];
+    U[e] = (i == j) ? v + (warm ? 0.0 : s) : v * isq2;
+    if (proj && !warm) V[e] = (i == j) ? 1.0 : 0.0;
+  }
+  if (warm) {
+    const double *Vp = a.Vstore + a.voff[bidx];
+    for (int e = tid; e < n * n; e += nt) V[e] = Vp[e];
+    __syncthreads();
+    constexpr int KM = 16;             // n*n <= KM * nt is checked at setup
+    double acc[KM];
+#pragma unroll
+    for (int k = 0; k < KM; ++k) {
+      const int e = tid + k * nt;
+      acc[k] = 0.0;
+      if (e < n * n) {
+        const int j = e / n, i = e - j * n;   // column j, row i
+        const double *vj = V + j * n;
+        double t = s * vj[i];
+        for (int q = 0; q < n; ++q) t += U[q * n + i] * vj[q];
+        acc[k] = t;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < KM; ++k) {
+      const int e = tid + k * nt;
+      if (e < n * n) U[e] = acc[k];
+    }
+  }
+  __syncthreads();
+  // ---- 3. one-sided Jacobi sweeps (round-robin pairs) ---------------------------------
+  // Column norms nrm[j] = ||u_j||^2 live in shared memory (recomputed exactly at the
+  // start of every sweep, updated per rotation), so a pair needs one dot u_p.u_q.
+  // The rotation angle is computed in fp32 (it only has to reduce u_p.u_q); (c, s) are
+  // then made orthogonal to fp64 precision, so V stays orthogonal.
+  double *nrm = lamv;             // reuses the eigenvalue slot until step 4
+  const double tol = fmax(a.tol, 4.0 * n * 2.220446049250313e-16);
+  const double tol2 = tol * tol, quad2 = 1e-18;   // quad: sweep with max |cos| < 1e-9 is final
+  bool converged = false;
+  int sweep = 0;
+  for (; sweep < a.max_sweeps; ++sweep) {
+    for (int j = warp; j < n; j += nwarps) {
+      const double *uj = U + j * n;
+      double t = 0.0;
+      for (int i = lane; i < n; i += 32) t += uj[i] * uj[i];
+      t = warp_sum(t);
+      if (lane == 0) nrm[j] = t;
+    }
+    __syncthreads();
+    int rotated = 0, big = 0;
+    for (int r = 0; r < NP - 1; ++r) {
+      for (int P0 = warp * PPW; P0 < H; P0 += nwarps * PPW) {
+        const int P = P0 + grp;
+        int p = 0, q = 0;
+        bool valid = P < H;
+        if (valid) {
+          p = rr_pos(P, r, NP - 1); q = rr_pos(NP - 1 - P, r, NP - 1);
+          if (p > q) { const int tmp = p; p = q; q = tmp; }
+          valid = q < n;                       // bye for odd n
+        }
+        double *up = U + p * n, *uq = U + q * n;
+        double xp[EPL], xq[EPL];
+        double ga = 0.0;
+#pragma unroll
+        for (int c = 0; c < EPL; ++c) {
+          const int i = sub + G * c;
+          const bool ok = valid && i < n;
+          xp[c] = ok ? up[i] : 0.0;
+          xq[c] = ok ? uq[i] : 0.0;
+          ga += xp[c] * xq[c];
+        }
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) ga += __shfl_xor_sync(0xffffffffu, ga, o);
+        const double al = valid ? nrm[p] : 1.0, be = valid ? nrm[q] : 1.0;
+        const double ab = al * be, g2a = ga * ga;
+        if (valid && ga != 0.0 && g2a > tol2 * ab) {
+          rotated = 1;
+          if (g2a > quad2 * ab) big = 1;
+          // tan(theta) zeroing u_p.u_q: t = sign(d) g2 / (|d| + sqrt(d^2 + g2^2)),
+          // d = be - al, g2 = 2 ga; evaluated in fp32 after exact power-of-2 scaling
+          const double d = be - al, g2 = 2.0 * ga;
+          const double mx = fmax(fabs(d), fabs(g2));
+          const int ex = ilogb(mx);
+          const float df = (float)scalbn(d, -ex), gf = (float)scalbn(g2, -ex);
+          const float tf = __fdividef(d >= 0.0 ? gf : -gf, fabsf(df) + sqrtf(df * df + gf * gf));
+          const double t = (double)tf;
+          const double y = 1.0 + t * t;
+          double cs = (double)rsqrtf((float)y);
+          cs = cs * (1.5 - 0.5 * y * cs * cs);
+          cs = cs * (1.5 - 0.5 * y * cs * cs);
+          const double sn = cs * t;
+#pragma unroll
+          for (int c = 0; c < EPL; ++c) {
+            const int i = sub + G * c;
+            if (i < n) { up[i] = cs * xp[c] - sn * xq[c]; uq[i] = sn * xp[c] + cs * xq[c]; }
+          }
+          if (sub == 0) {   // exact norms of the rotated pair from the 2x2 Gram matrix
+            const double c2 = cs * cs, s2 = sn * sn, csn = 2.0 * cs * sn * ga;
+            nrm[p] = c2 * al - csn + s2 * be;
+            nrm[q] = s2 * al + csn + c2 * be;
+          }
+          if (proj) {
+            double *vp = V + p * n, *vq = V + q * n;
+#pragma unroll
+            for (int c = 0; c < EPL; ++c) {
+              const int i = sub + G * c;
+              if (i < n) {
+                const double a0 = vp[i], b0 = vq[i];
+                vp[i] = cs * a0 - sn * b0; vq[i] = sn * a0 + cs * b0;
+              }
+            }
+          }
+        }
+      }
+      __syncthreads();
+    }
+    const int any_big = __syncthreads_or(big);
+    const int any_rot = __syncthreads_or(rotated);
+    if (!any_rot || !any_big) { converged = true; break; }
+  }
+  if (tid == 0) {
+    if (!converged) atomicCAS(&a.st->eig_fail, 0, bidx + 1);
+    atomicAdd(&a.st->eig_sweeps, (unsigned long long)(sweep + 1));
+  }
+  // ---- 4. eigenvalues lambda_j = ||u_j|| - s  (u_j = (lambda_j + s) v_j) ------------------
+  for (int j = warp; j < n; j += nwarps) {
+    const double *uj = U + j * n;
+    double nn = 0.0;
+    for (int i = lane; i < n; i += 32) nn += uj[i] * uj[i];
+    nn = warp_sum(nn);
+    if (lane == 0) lamv[j] = sqrt(nn) - s;
+  }
+  __syncthreads();
+  const double *lam = lamv;
+  if (!proj) {
+    if (tid == 0) {
+      double lm = lam[0];
+      for (int k = 1; k < n; ++k) lm = fmin(lm, lam[k]);
+      a.lam_min[bidx] = lm;
+    }
+    return;
+  }
+  if (tid == 0) {
+    int npos = 0, nneg = 0;
+    for (int k = 0; k < n; ++k) { if (lam[k] > 0.0) ++npos; else if (lam[k] < 0.0) ++nneg; }
+    const int use_pos = npos <= nneg;
+    int cnt = 0;
+    for (int k = 0; k < n; ++k)
+      if (use_pos ? (lam[k] > 0.0) : (lam[k] < 0.0)) sets[cnt++] = k;
+    set_info = cnt * 2 + use_pos;
+  }
+  __syncthreads();
+  const int cnt = set_info >> 1, use_pos = set_info & 1;
+  const double is = 1.0 / sigma;
+  // ---- 5. S = (Pi(X_b) - X_b)/sigma in svec ------------------------------------------
+  for (int e = tid; e < L; e += nt) {
+    int j = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+    while (j * (j + 1) / 2 > e) --j;
+    while ((j + 1) * (j + 2) / 2 <= e) ++j;
+    const int i = e - j * (j + 1) / 2;
+    double acc = 0.0;
+    for (int c = 0; c < cnt; ++c) {
+      const int k = sets[c];
+      acc += lam[k] * V[k * n + i] * V[k * n + j];
+    }
+    double sv;
+    if (use_pos) {
+      const double xb = Xb[e];
+      sv = (acc - (i == j ? xb : xb * isq2)) * is;
+    } else {
+      sv = -acc * is;
+    }
+    a.S_out[off + e] = (i == j) ? sv : sv * 1.41421356237309504880;
+  }
+  // ---- 6. keep the eigenbasis for the next iteration -------------------------------
+  double *Vs = a.Vstore + a.voff[bidx];
+  for (int e = tid; e < n * n; e += nt) Vs[e] = V[e];
+}
+
+inline size_t eig_smem_bytes(int n) { return sizeof(double) * (2 * (size_t)n * n + n + 8); }
+
+// lanes per pair and launch shape for a block of order n
+inline int eig_G(int n) { return n <= 16 ? 4 : (n <= 64 ? 8 : 16); }
+inline int eig_threads(int n) {
+  const int H = (n + (n & 1)) / 2, G = eig_G(n), ppw = 32 / G;
+  int warps = (H + ppw - 1) / ppw;
+  int t = 32 * std::max(warps, 1);
+  while (t < 512 && (int64_t)n * n > 16LL * t) t += 32;   // warm-start product capacity
+  if (n > 16) t = std::max(t, 256);
+  return std::min(t, 512);
+}

@@ -74,6 +74,20 @@ __device__ __forceinline__ double rhs(const RhsArgs &a, double inv_sigma, int i)
   return (a.b[i] - a.ax[i]) * inv_sigma - a.as[i] + a.ac[i];
 }
 
+// Warp dot product sum_{j in [lo,hi)} a[j] x[j], 4 independent loads in flight per lane.
+__device__ __forceinline__ double warp_dot(const double *__restrict__ a, const double *__restrict__ x,
+                                           int lo, int hi, int lane) {
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  int j = lo + lane;
+  for (; j + 96 < hi; j += 128) {
+    const double a0 = __ldg(a + j), a1 = __ldg(a + j + 32), a2 = __ldg(a + j + 64), a3 = __ldg(a + j + 96);
+    const double x0 = x[j], x1 = x[j + 32], x2 = x[j + 64], x3 = x[j + 96];
+    s0 += a0 * x0; s1 += a1 * x1; s2 += a2 * x2; s3 += a3 * x3;
+  }
+  for (; j < hi; j += 32) s0 += __ldg(a + j) * x[j];
+  return warp_sum((s0 + s1) + (s2 + s3));
+}
+
 // ============================ K-TRSV phases ================================
 // P1: u_Q = r_Q - G r_L            (leaf elimination, forward)
 __global__ void k_solve_p1(SolveDev d, RhsArgs ra, const DevState *st) {
@@ -108,7 +122,19 @@ __global__ void k_gemv_stage(SolveDev d, const GemvItem *items, int nitems, cons
     base[c] = c < it.cnt ? d.R_off[stage_list[it.list + c]] : 0;
     acc[c] = 0.0;
   }
-  for (int j = jlo + lane; j < jhi; j += 32) {
+  if (it.cnt == 1) {   // unique (non-shared) factor: plain unrolled dot
+    const double s = warp_dot(M, in + base[0], jlo, jhi, lane);
+    if (lane == 0) out[base[0] + it.row] = s;
+    return;
+  }
+  int j = jlo + lane;
+  for (; j + 32 < jhi; j += 64) {
+    const double m0 = __ldg(M + j), m1 = __ldg(M + j + 32);
+#pragma unroll
+    for (int c = 0; c < kGemvChunk; ++c)
+      if (c < it.cnt) acc[c] += m0 * in[base[c] + j] + m1 * in[base[c] + j + 32];
+  }
+  for (; j < jhi; j += 32) {
     const double mij = __ldg(M + j);
 #pragma unroll
     for (int c = 0; c < kGemvChunk; ++c)
@@ -138,15 +164,14 @@ __global__ void k_solve_p3(SolveDev d, const DevState *st) {
     const double *Ft = d.Ft[uid] + (int64_t)(d.stage_wl[k] + c) * nk;
     const double *vk = d.v + d.R_off[k];
     (void)wk;
-    for (int i = lane; i < nk; i += 32) acc += __ldg(Ft + i) * vk[i];
+    acc += warp_dot(Ft, vk, 0, nk, lane);
   }
   {  // stage j+1: its left separator is S_j -> F column c
     const int k = j + 1, uid = d.stage_uid[k], nk = d.uid_n[uid];
     const double *Ft = d.Ft[uid] + (int64_t)c * nk;
     const double *vk = d.v + d.R_off[k];
-    for (int i = lane; i < nk; i += 32) acc += __ldg(Ft + i) * vk[i];
+    acc += warp_dot(Ft, vk, 0, nk, lane);
   }
-  acc = warp_sum(acc);
   if (lane == 0) d.u[s] -= acc;
 }
 
@@ -161,14 +186,12 @@ __global__ void k_solve_sep(SolveDev d, int mode, double *y, const DevState *st)
   if (mode == 0) {
     const double *M = d.LTinv + (int64_t)w * n;
     const double *x = d.u + d.S0;
-    for (int j = lane; j <= w; j += 32) acc += __ldg(M + j) * x[j];
-    acc = warp_sum(acc);
+    acc = warp_dot(M, x, 0, w + 1, lane);
     if (lane == 0) d.z[d.S0 + w] = acc;
   } else {
     const double *M = d.LTinvT + (int64_t)w * n;
     const double *x = d.z + d.S0;
-    for (int j = w + lane; j < n; j += 32) acc += __ldg(M + j) * x[j];
-    acc = warp_sum(acc);
+    acc = warp_dot(M, x, w, n, lane);
     if (lane == 0) y[d.S0 + w] = acc;
   }
 }
@@ -208,200 +231,7 @@ __global__ void k_solve_p7(SolveDev d, RhsArgs ra, double *y, const DevState *st
 }
 
 // ============================ K-EIG =========================================
-// One CTA per PSD block: gather X_b = X + sigma (A* y - C) (Step 2, fused A*),
-// parallel-order cyclic two-sided Jacobi in shared memory (fp64), then
-// S = (Pi(X_b) - X_b)/sigma with Pi = Q max(0,W) Q^T,
-// reconstructed from the smaller of the positive / negative eigen-sets.
-struct EigArgs {
-  const int32_t *blocks; int32_t nblk;
-  const int32_t *bn; const int64_t *boff;
-  const int64_t *Atp; const int32_t *Atr; const double *Atv;
-  const double *X, *C, *y;
-  double *Xb_out, *S_out;
-  DevState *st;
-  int32_t max_sweeps; double tol;
-  int32_t mode;          // 0 projection; 1 eigenvalues of C - A*y (lambda_min only)
-  double *lam_min;
-};
-
-__device__ __forceinline__ void pair_of(int P, int r, int NP, int &p, int &q) {
-  auto pos = [&](int j) { return j == 0 ? 0 : 1 + ((j - 1 + r) % (NP - 1)); };
-  p = pos(P); q = pos(NP - 1 - P);
-}
-
-__device__ __forceinline__ void jacobi_rot(double app, double aqq, double apq, double &c, double &s,
-                                           double &t) {
-  if (apq == 0.0) { c = 1.0; s = 0.0; t = 0.0; return; }
-  const double theta = (aqq - app) / (2.0 * apq);
-  const double at = fabs(theta);
-  double tt;
-  if (at > 1e150) tt = 0.5 / theta;
-  else tt = (theta >= 0.0 ? 1.0 : -1.0) / (at + sqrt(1.0 + theta * theta));
-  c = rsqrt(1.0 + tt * tt);
-  s = tt * c;
-  t = tt;
-}
-
-__global__ void k_eig(EigArgs a) {
-  if (a.st->done) return;
-  extern __shared__ double sm[];
-  const int bidx = a.blocks[blockIdx.x];
-  const int n = a.bn[bidx];
-  const int NP = n + (n & 1);
-  const int H = NP / 2;
-  const int64_t off = a.boff[bidx];
-  const int L = n * (n + 1) / 2;
-  double *A = sm;                       // NP x NP
-  double *V = A + NP * NP;              // n x NP
-  double *rot = V + n * NP;             // 3 * H
-  double *red = rot + 3 * H;            // 64 scratch
-  int *sets = (int *)(red + 64);        // NP ints (+1 count)
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const double sigma = a.st->sigma;
-  const double isq2 = 0.70710678118654752440;
-  for (int e = tid; e < NP * NP; e += nt) A[e] = 0.0;
-  __syncthreads();
-  // ---- gather X_b (or C - A*y) --------------------------------------------
-  for (int e = tid; e < L; e += nt) {
-    const int64_t J = off + e;
-    double aty = 0.0;
-    for (int64_t t = a.Atp[J]; t < a.Atp[J + 1]; ++t) aty += a.Atv[t] * a.y[a.Atr[t]];
-    double xb;
-    if (a.mode == 0) {
-      xb = a.X[J] + sigma * (aty - a.C[J]);
-      a.Xb_out[J] = xb;
-    } else {
-      xb = a.C[J] - aty;
-    }
-    int j = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
-    while (j * (j + 1) / 2 > e) --j;
-    while ((j + 1) * (j + 2) / 2 <= e) ++j;
-    const int i = e - j * (j + 1) / 2;
-    const double v = (i == j) ? xb : xb * isq2;
-    A[i * NP + j] = v;
-    A[j * NP + i] = v;
-  }
-  const bool want_vec = (a.mode == 0);
-  if (want_vec)
-    for (int e = tid; e < n * NP; e += nt) V[e] = ((e / NP) == (e % NP)) ? 1.0 : 0.0;
-  __syncthreads();
-  // ---- Jacobi sweeps ----------------------------------------------------------
-  int sweep = 0;
-  bool converged = false;
-  for (; sweep <= a.max_sweeps; ++sweep) {
-    // off-norm test
-    double v2[2] = {0.0, 0.0};
-    for (int e = tid; e < NP * NP; e += nt) {
-      const double x = A[e];
-      v2[0] += x * x;
-      if ((e / NP) != (e % NP)) v2[1] += x * x;
-    }
-    block_sum<2>(v2, red);
-    if (tid == 0) red[63] = (v2[1] <= a.tol * a.tol * v2[0]) ? 1.0 : 0.0;
-    __syncthreads();
-    if (red[63] != 0.0) { converged = true; break; }
-    if (sweep == a.max_sweeps) break;
-    __syncthreads();
-    for (int r = 0; r < NP - 1; ++r) {
-      for (int P = tid; P < H; P += nt) {
-        int p, q; pair_of(P, r, NP, p, q);
-        double c, s, t;
-        jacobi_rot(A[p * NP + p], A[q * NP + q], A[p * NP + q], c, s, t);
-        rot[3 * P] = c; rot[3 * P + 1] = s; rot[3 * P + 2] = t;
-      }
-      __syncthreads();
-      const int nA = H * H;
-      const int nV = want_vec ? n * H : 0;
-      for (int item = tid; item < nA + nV; item += nt) {
-        if (item < nA) {
-          const int P = item / H, R = item % H;
-          if (P > R) continue;
-          int p, q, rr, ss;
-          pair_of(P, r, NP, p, q);
-          pair_of(R, r, NP, rr, ss);
-          const double cP = rot[3 * P], sP = rot[3 * P + 1];
-          if (P == R) {
-            const double tP = rot[3 * P + 2], apq = A[p * NP + q];
-            A[p * NP + p] -= tP * apq;
-            A[q * NP + q] += tP * apq;
-            A[p * NP + q] = 0.0;
-            A[q * NP + p] = 0.0;
-          } else {
-            const double cR = rot[3 * R], sR = rot[3 * R + 1];
-            const double b00 = A[p * NP + rr], b01 = A[p * NP + ss];
-            const double b10 = A[q * NP + rr], b11 = A[q * NP + ss];
-            // W = B J_R
-            const double w00 = cR * b00 - sR * b01, w01 = sR * b00 + cR * b01;
-            const double w10 = cR * b10 - sR * b11, w11 = sR * b10 + cR * b11;
-            // B' = J_P^T W
-            const double n00 = cP * w00 - sP * w10, n01 = cP * w01 - sP * w11;
-            const double n10 = sP * w00 + cP * w10, n11 = sP * w01 + cP * w11;
-            A[p * NP + rr] = n00; A[p * NP + ss] = n01;
-            A[q * NP + rr] = n10; A[q * NP + ss] = n11;
-            A[rr * NP + p] = n00; A[ss * NP + p] = n01;
-            A[rr * NP + q] = n10; A[ss * NP + q] = n11;
-          }
-        } else {
-          const int e = item - nA;
-          const int i = e / H, P = e % H;
-          int p, q; pair_of(P, r, NP, p, q);
-          const double cP = rot[3 * P], sP = rot[3 * P + 1];
-          const double vp = V[i * NP + p], vq = V[i * NP + q];
-          V[i * NP + p] = cP * vp - sP * vq;
-          V[i * NP + q] = sP * vp + cP * vq;
-        }
-      }
-      __syncthreads();
-    }
-  }
-  if (!converged && tid == 0) atomicCAS(&a.st->eig_fail, 0, bidx + 1);
-  // ---- eigenvalue sets ----------------------------------------------------------
-  if (a.mode == 1) {
-    if (tid == 0) {
-      double lm = A[0];
-      for (int k = 1; k < n; ++k) lm = fmin(lm, A[k * NP + k]);
-      a.lam_min[bidx] = lm;
-    }
-    return;
-  }
-  if (tid == 0) {
-    int npos = 0, nneg = 0;
-    for (int k = 0; k < NP; ++k) {
-      const double lk = A[k * NP + k];
-      if (lk > 0.0) ++npos; else if (lk < 0.0) ++nneg;
-    }
-    const int use_pos = npos <= nneg;
-    int cnt = 0;
-    for (int k = 0; k < NP; ++k) {
-      const double lk = A[k * NP + k];
-      if (use_pos ? (lk > 0.0) : (lk < 0.0)) sets[1 + cnt++] = k;
-    }
-    sets[0] = cnt * 2 + use_pos;
-  }
-  __syncthreads();
-  const int cnt = sets[0] >> 1, use_pos = sets[0] & 1;
-  const double is = 1.0 / sigma;
-  for (int e = tid; e < L; e += nt) {
-    int j = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
-    while (j * (j + 1) / 2 > e) --j;
-    while ((j + 1) * (j + 2) / 2 <= e) ++j;
-    const int i = e - j * (j + 1) / 2;
-    double acc = 0.0;
-    for (int c = 0; c < cnt; ++c) {
-      const int k = sets[1 + c];
-      acc += A[k * NP + k] * V[i * NP + k] * V[j * NP + k];
-    }
-    double sv;
-    if (use_pos) {   // S = (sum_{l>0} l v v^T - X_b) / sigma
-      const double xb = a.Xb_out[off + e];
-      const double xm = (i == j) ? xb : xb * isq2;
-      sv = (acc - xm) * is;
-    } else {         // S = sum_{l<0} (-l) v v^T / sigma   (Moreau)
-      sv = -acc * is;
-    }
-    a.S_out[off + e] = (i == j) ? sv : sv * 1.41421356237309504880;
-  }
-}
+#include "eig.cuh"
 
 // ============================ K-SPMV / K-FUSE ==================================
 // AS = A S  (thread per row, internal row order)
@@ -489,6 +319,7 @@ __global__ void k_finalize(const double *part_ax, int nax, const double *part_up
       st->sigma = sg;
     }
     const double eta = fmax(eta_p, fmax(eta_d, eta_g));
+    st->eig_warm_valid = 1;   // every block's eigenbasis was stored by this iteration
     if ((st->tol >= 0.0 && eta <= st->tol) || st->nan_flag) st->done = 1;
   }
 }
@@ -544,6 +375,7 @@ struct strom_admm {
   int K = 50;
   int launches_per_iter = 0;
   double *lam_dev = nullptr;
+  double *Vstore = nullptr; int64_t *voff = nullptr;
   // per-kernel event instrumentation of one iteration inside the K-graph
   std::vector<cudaEvent_t> prof_ev;
   std::vector<const char *> prof_names;
@@ -628,9 +460,6 @@ strom_status launch_solve(strom_admm *h, const RhsArgs &ra, double *y, int &nl) 
   return STROM_OK;
 }
 
-size_t eig_smem(int np, int n) {
-  return sizeof(double) * ((size_t)np * np + (size_t)n * np + 3 * (np / 2) + 64) + sizeof(int) * (np + 2);
-}
 
 strom_status launch_eig(strom_admm *h, int mode, const double *yv, int &nl) {
   nl = 0;
@@ -644,12 +473,17 @@ strom_status launch_eig(strom_admm *h, int mode, const double *yv, int &nl) {
     a.Xb_out = h->Xb; a.S_out = h->S; a.st = h->st;
     a.max_sweeps = h->cfg.eig_max_sweeps; a.tol = h->cfg.eig_tol;
     a.mode = mode; a.lam_min = h->lam_dev;
-    const int threads = np <= 16 ? 64 : (np <= 64 ? 256 : 512);
-    const size_t smem = eig_smem(np, np);
+    a.Vstore = h->Vstore; a.voff = h->voff;
+    a.warm_enable = h->cfg.eig_warm; a.cold_every = h->cfg.eig_cold_every;
+    const int threads = eig_threads(np);
+    const size_t smem = eig_smem_bytes(np);
     static const char *eig_names[] = {"eig_class0", "eig_class1", "eig_class2", "eig_class3",
                                       "eig_class4", "eig_class5", "eig_class6", "eig_class7"};
     mark(h, eig_names[c < 8 ? c : 7]);
-    k_eig<<<a.nblk, threads, smem, h->stream>>>(a);
+    const int G = eig_G(np);
+    if (G == 4) k_eig<4, 4><<<a.nblk, threads, smem, h->stream>>>(a);
+    else if (G == 8) k_eig<8, 8><<<a.nblk, threads, smem, h->stream>>>(a);
+    else k_eig<16, 8><<<a.nblk, threads, smem, h->stream>>>(a);
     ++nl;
   }
   CK(cudaGetLastError());
@@ -722,6 +556,7 @@ strom_status reset_state(strom_admm *h) {
   DevState old{};
   CK(cudaMemcpy(&old, h->st, sizeof(DevState), cudaMemcpyDeviceToHost));
   nb = old.normb; nc = old.normC;
+  ds.eig_sweeps = old.eig_sweeps;
   ds.normb = nb; ds.normC = nc;
   ds.sigma_used = ds.sigma;
   CK(cudaMemcpy(h->st, &ds, sizeof(DevState), cudaMemcpyHostToDevice));
@@ -918,12 +753,17 @@ strom_status strom_admm_setup(strom_admm **out, const strom_sdp *sdp_h, const st
       int32_t *pd;
       if ((st = h->upload(pd, h->eig_class_blocks[c]))) return st;
       h->eig_class_dev.push_back(pd);
-      const size_t smem = eig_smem(nps[c], nps[c]);
-      if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_eig, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 48 * 1024)));
     }
     size_t maxsm = 0;
-    for (int np : nps) maxsm = std::max(maxsm, eig_smem(np, np));
-    if (maxsm > 48 * 1024) CK(cudaFuncSetAttribute(k_eig, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)maxsm));
+    for (int np : nps) maxsm = std::max(maxsm, eig_smem_bytes(np));
+    std::vector<int64_t> voff(s.nblocks + 1, 0);
+    for (int k = 0; k < s.nblocks; ++k) voff[k + 1] = voff[k] + (int64_t)s.bn[k] * s.bn[k];
+    if ((st = h->upload(h->voff, voff)) || (st = h->alloc(h->Vstore, voff[s.nblocks]))) return st;
+    if (maxsm > 48 * 1024) {
+      CK(cudaFuncSetAttribute(k_eig<4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)maxsm));
+      CK(cudaFuncSetAttribute(k_eig<8, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)maxsm));
+      CK(cudaFuncSetAttribute(k_eig<16, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)maxsm));
+    }
   }
   // ---- state, AC = A C, norms -------------------------------------------------
   {
@@ -1036,6 +876,7 @@ strom_status strom_admm_get(strom_admm *h, double *X, double *y, double *S, stro
   if (res) {
     res->iter = ds.iter; res->eta_p = ds.eta_p; res->eta_d = ds.eta_d; res->eta_g = ds.eta_g;
     res->pobj = ds.pobj; res->dobj = ds.dobj; res->sigma = ds.sigma_used; res->eta_x = ds.eta_x;
+    res->eig_sweeps = (int64_t)ds.eig_sweeps;
   }
   if (ds.eig_fail) {
     set_error("Jacobi sweep cap reached on block " + std::to_string(ds.eig_fail - 1));
@@ -1128,7 +969,8 @@ strom_status strom_debug_project_psd(strom_admm *h, const double *Xb, double sig
   CK(cudaMemcpy(&ds, h->st, sizeof(DevState), cudaMemcpyDeviceToHost));
   const double sg_old = ds.sigma;
   const int32_t done_old = ds.done;
-  ds.sigma = sigma; ds.done = 0;
+  const int32_t warm_old = ds.eig_warm_valid;
+  ds.sigma = sigma; ds.done = 0; ds.eig_warm_valid = 0;
   CK(cudaMemcpy(h->st, &ds, sizeof(DevState), cudaMemcpyHostToDevice));
   h->X = h->tmp_m; h->C = h->tmp_m2;
   int nl = 0;
@@ -1143,7 +985,7 @@ strom_status strom_debug_project_psd(strom_admm *h, const double *Xb, double sig
   }
   CK(cudaMemcpy(&ds, h->st, sizeof(DevState), cudaMemcpyDeviceToHost));
   const int32_t fail = ds.eig_fail;
-  ds.sigma = sg_old; ds.done = done_old; ds.eig_fail = 0;
+  ds.sigma = sg_old; ds.done = done_old; ds.eig_fail = 0; ds.eig_warm_valid = warm_old;
   CK(cudaMemcpy(h->st, &ds, sizeof(DevState), cudaMemcpyHostToDevice));
   // restore S of the iterate is not needed for tests (they reset with set_start)
   if (fail) { set_error("Jacobi sweep cap reached"); return STROM_EEIG; }

@@ -17,6 +17,8 @@ struct DevState {          // scalars living on the device
   int32_t eig_fail;        // Jacobi exceeded its sweep cap (block id + 1)
   int32_t nan_flag;
   int32_t sigma_period;
+  int32_t eig_warm_valid;  // 1 once every block has a stored eigenbasis
+  unsigned long long eig_sweeps;   // diagnostic: Jacobi sweeps summed over blocks
   double sigma_ratio, sigma_factor, sigma_min, sigma_max;
   // residuals of the latest completed iterate
   double eta_p, eta_d, eta_g, pobj, dobj, eta_x, sigma_used;

@@ -13,10 +13,13 @@ for N in (5, 30):
     t2 = time.time()
     print(f"N={N} gen {t1-t0:.2f}s setup {t2-t1:.2f}s", g.factor_info(), "launches/iter", g.launches_per_iter(), flush=True)
     g.iterate(100); torch.cuda.synchronize()
+    sw0 = g.residuals()["eig_sweeps"]
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(); g.iterate(1000); e1.record(); torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / 1000
-    print(f"N={N}: {ms*1000:.1f} us/iter, {1000/ms:.0f} iters/s", g.residuals(), flush=True)
+    r = g.residuals()
+    print(f"N={N}: {ms*1000:.1f} us/iter, {1000/ms:.0f} iters/s, sweeps/block/iter {(r['eig_sweeps']-sw0)/1000/sdp.nblocks:.2f}", r, flush=True)
+    print([(a, round(b*1000,1)) for a,b in g.kernel_times()], flush=True)
     ok, it = g.solve(1e-6, 100000 if N == 5 else 20000)
     torch.cuda.synchronize()
     print("solve", ok, it, g.residuals(), flush=True)
