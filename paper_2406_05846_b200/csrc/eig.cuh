@@ -1,7 +1,7 @@
 // K-EIG: batched PSD-cone projection (Step 2 of Algorithm 1, PAPER.md:467-472;
 // projection Pi(X) = Q max(0, W) Q^T), included by engine.cu.
 //
-// One CTA per PSD block X_beta (order n <= 118), fp64 throughout:
+// One CTA per PSD block X_beta (order n <= 112), fp64 throughout:
 //   1. gather X_b = X + sigma (A* y - C) straight from svec (A* fused);
 //   2. one-sided (Hestenes) Jacobi on the shifted matrix B = X_b + s I, s = ||X_b||_F,
 //      so that B is PSD with eigenvalues lambda + s >= 0 kept apart even when X_b has
@@ -36,6 +36,18 @@ __device__ __forceinline__ int rr_pos(int j, int r, int NPm1) {
   return 1 + t;
 }
 
+// fp64 MUFU approximations (~20 bits) refined by Newton steps: no f64<->f32 conversions.
+__device__ __forceinline__ double rsqrt_approx(double x) {
+  double r;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  return r;
+}
+__device__ __forceinline__ double rcp_approx(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  return r;
+}
+
 __device__ __forceinline__ int svec_pos(int i, int j) {  // i, j any order
   return (i <= j) ? (j * (j + 1) / 2 + i) : (i * (i + 1) / 2 + j);
 }
@@ -57,6 +69,7 @@ __global__ void __launch_bounds__(512, 1) k_eig(EigArgs a) {
   double *U = sm;                 // n columns x n rows, column-major (column j at U + j*n)
   double *V = sm + n * n;         // same layout
   double *lamv = sm + 2 * n * n;  // n eigenvalues
+  unsigned short *sched = (unsigned short *)(lamv + n + 8);  // (p | q << 8) per (round, pair)
   const int tid = threadIdx.x, nt = blockDim.x;
   const int lane = tid & 31, warp = tid >> 5, nwarps = nt >> 5;
   const int grp = lane / G, sub = lane % G;
@@ -65,6 +78,12 @@ __global__ void __launch_bounds__(512, 1) k_eig(EigArgs a) {
   const bool proj = (a.mode == 0);
   const bool warm = proj && a.warm_enable && a.st->eig_warm_valid && n * n <= 16 * nt &&
                     (a.cold_every <= 0 || (a.st->iter % a.cold_every) != 0);
+  for (int e = tid; e < (NP - 1) * H; e += nt) {
+    const int r = e / H, P = e - r * H;
+    int p = rr_pos(P, r, NP - 1), q = rr_pos(NP - 1 - P, r, NP - 1);
+    if (p > q) { const int t2 = p; p = q; q = t2; }
+    sched[e] = (unsigned short)(p | (q << 8));
+  }
   // ---- 1. gather X_b (svec) into global, Frobenius norm -------------------------
   double fro = 0.0;
   for (int e = tid; e < L; e += nt) {
@@ -142,21 +161,22 @@ __global__ void __launch_bounds__(512, 1) k_eig(EigArgs a) {
         int p = 0, q = 0;
         bool valid = P < H;
         if (valid) {
-          p = rr_pos(P, r, NP - 1); q = rr_pos(NP - 1 - P, r, NP - 1);
-          if (p > q) { const int tmp = p; p = q; q = tmp; }
+          const unsigned pq = sched[r * H + P];
+          p = pq & 0xff; q = pq >> 8;
           valid = q < n;                       // bye for odd n
         }
         double *up = U + p * n, *uq = U + q * n;
         double xp[EPL], xq[EPL];
-        double ga = 0.0;
+        double ga0 = 0.0, ga1 = 0.0;
 #pragma unroll
         for (int c = 0; c < EPL; ++c) {
           const int i = sub + G * c;
           const bool ok = valid && i < n;
           xp[c] = ok ? up[i] : 0.0;
           xq[c] = ok ? uq[i] : 0.0;
-          ga += xp[c] * xq[c];
+          if (c & 1) ga1 += xp[c] * xq[c]; else ga0 += xp[c] * xq[c];
         }
+        double ga = ga0 + ga1;
 #pragma unroll
         for (int o = G / 2; o > 0; o >>= 1) ga += __shfl_xor_sync(0xffffffffu, ga, o);
         const double al = valid ? nrm[p] : 1.0, be = valid ? nrm[q] : 1.0;
@@ -165,17 +185,26 @@ __global__ void __launch_bounds__(512, 1) k_eig(EigArgs a) {
           rotated = 1;
           if (g2a > quad2 * ab) big = 1;
           // tan(theta) zeroing u_p.u_q: t = sign(d) g2 / (|d| + sqrt(d^2 + g2^2)),
-          // d = be - al, g2 = 2 ga; evaluated in fp32 after exact power-of-2 scaling
+          // d = be - al, g2 = 2 ga. t needs only ~1e-10 relative accuracy (it just has to
+          // shrink u_p.u_q); (cs, sn) are exactly orthogonal to fp64 precision.
           const double d = be - al, g2 = 2.0 * ga;
-          const double mx = fmax(fabs(d), fabs(g2));
-          const int ex = ilogb(mx);
-          const float df = (float)scalbn(d, -ex), gf = (float)scalbn(g2, -ex);
-          const float tf = __fdividef(d >= 0.0 ? gf : -gf, fabsf(df) + sqrtf(df * df + gf * gf));
-          const double t = (double)tf;
-          const double y = 1.0 + t * t;
-          double cs = (double)rsqrtf((float)y);
-          cs = cs * (1.5 - 0.5 * y * cs * cs);
-          cs = cs * (1.5 - 0.5 * y * cs * cs);
+          const double h2 = fma(d, d, g2 * g2);
+          double rh = rsqrt_approx(h2);
+          rh = rh * fma(-0.5 * h2, rh * rh, 1.5);
+          const double den = fabs(d) + h2 * rh;
+          double rc = rcp_approx(den);
+          rc = rc * fma(-den, rc, 2.0);
+          const double t = (d >= 0.0 ? g2 : -g2) * rc;
+          const double t2 = t * t;
+          double cs;
+          if (t2 < 1e-8) {          // cos = (1 + t^2)^(-1/2), series exact to 1e-24
+            cs = fma(t2, fma(t2, 0.375, -0.5), 1.0);
+          } else {
+            const double y = 1.0 + t2;
+            cs = rsqrt_approx(y);
+            cs = cs * fma(-0.5 * y, cs * cs, 1.5);
+            cs = cs * fma(-0.5 * y, cs * cs, 1.5);
+          }
           const double sn = cs * t;
 #pragma unroll
           for (int c = 0; c < EPL; ++c) {
@@ -265,10 +294,18 @@ __global__ void __launch_bounds__(512, 1) k_eig(EigArgs a) {
   for (int e = tid; e < n * n; e += nt) Vs[e] = V[e];
 }
 
-inline size_t eig_smem_bytes(int n) { return sizeof(double) * (2 * (size_t)n * n + n + 8); }
+inline size_t eig_smem_bytes(int n) {
+  const int NP = n + (n & 1);
+  return sizeof(double) * (2 * (size_t)n * n + n + 8) + sizeof(unsigned short) * (size_t)(NP - 1) * (NP / 2) + 16;
+}
 
 // lanes per pair and launch shape for a block of order n
-inline int eig_G(int n) { return n <= 16 ? 4 : (n <= 64 ? 8 : 16); }
+inline int eig_G(int n) {
+  static int force = [] { const char *e = getenv("STROM_EIG_G"); return e ? atoi(e) : 0; }();
+  if (force == 8 && n <= 64) return 8;
+  if (force == 16 && n > 16) return 16;
+  return n <= 16 ? 4 : (n <= 64 ? 8 : 16);
+}
 inline int eig_threads(int n) {
   const int H = (n + (n & 1)) / 2, G = eig_G(n), ppw = 32 / G;
   int warps = (H + ppw - 1) / ppw;

@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -370,6 +371,9 @@ struct strom_admm {
   std::vector<std::vector<int32_t>> eig_class_blocks;
   std::vector<int32_t *> eig_class_dev;
   std::vector<int> eig_class_np;
+  int eig_main_class = 0;                    // class with the largest n^3 work
+  cudaStream_t stream2 = nullptr;            // fork for concurrent eig size classes
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   cudaGraph_t graphK = nullptr, graph1 = nullptr;
   cudaGraphExec_t execK = nullptr, exec1 = nullptr;
   int K = 50;
@@ -383,6 +387,9 @@ struct strom_admm {
   int prof_idx = 0, prof_count = 0;
   ~strom_admm() {
     for (cudaEvent_t e : prof_ev) cudaEventDestroy(e);
+    if (fork_ev) cudaEventDestroy(fork_ev);
+    if (join_ev) cudaEventDestroy(join_ev);
+    if (stream2) cudaStreamDestroy(stream2);
     if (execK) cudaGraphExecDestroy(execK);
     if (exec1) cudaGraphExecDestroy(exec1);
     if (graphK) cudaGraphDestroy(graphK);
@@ -462,8 +469,18 @@ strom_status launch_solve(strom_admm *h, const RhsArgs &ra, double *y, int &nl) 
 
 
 strom_status launch_eig(strom_admm *h, int mode, const double *yv, int &nl) {
+  // Size classes are independent: the largest class runs on the main stream, the
+  // others on a forked stream, joined before the next step (parallel graph branches).
   nl = 0;
-  for (size_t c = 0; c < h->eig_class_blocks.size(); ++c) {
+  const int ncls = (int)h->eig_class_blocks.size();
+  const bool fork = ncls > 1 && h->stream2;
+  if (fork) {
+    CK(cudaEventRecord(h->fork_ev, h->stream));
+    CK(cudaStreamWaitEvent(h->stream2, h->fork_ev, 0));
+  }
+  static const char *eig_names[] = {"eig_class0", "eig_class1", "eig_class2", "eig_class3",
+                                    "eig_class4", "eig_class5", "eig_class6", "eig_class7"};
+  for (int c = 0; c < ncls; ++c) {
     const int np = h->eig_class_np[c];
     EigArgs a;
     a.blocks = h->eig_class_dev[c]; a.nblk = (int)h->eig_class_blocks[c].size();
@@ -477,14 +494,17 @@ strom_status launch_eig(strom_admm *h, int mode, const double *yv, int &nl) {
     a.warm_enable = h->cfg.eig_warm; a.cold_every = h->cfg.eig_cold_every;
     const int threads = eig_threads(np);
     const size_t smem = eig_smem_bytes(np);
-    static const char *eig_names[] = {"eig_class0", "eig_class1", "eig_class2", "eig_class3",
-                                      "eig_class4", "eig_class5", "eig_class6", "eig_class7"};
-    mark(h, eig_names[c < 8 ? c : 7]);
+    cudaStream_t s = (fork && c != h->eig_main_class) ? h->stream2 : h->stream;
+    if (s == h->stream) mark(h, eig_names[c < 8 ? c : 7]);
     const int G = eig_G(np);
-    if (G == 4) k_eig<4, 4><<<a.nblk, threads, smem, h->stream>>>(a);
-    else if (G == 8) k_eig<8, 8><<<a.nblk, threads, smem, h->stream>>>(a);
-    else k_eig<16, 8><<<a.nblk, threads, smem, h->stream>>>(a);
+    if (G == 4) k_eig<4, 4><<<a.nblk, threads, smem, s>>>(a);
+    else if (G == 8) k_eig<8, 8><<<a.nblk, threads, smem, s>>>(a);
+    else k_eig<16, 8><<<a.nblk, threads, smem, s>>>(a);
     ++nl;
+  }
+  if (fork) {
+    CK(cudaEventRecord(h->join_ev, h->stream2));
+    CK(cudaStreamWaitEvent(h->stream, h->join_ev, 0));
   }
   CK(cudaGetLastError());
   return STROM_OK;
@@ -594,8 +614,8 @@ strom_status strom_admm_setup(strom_admm **out, const strom_sdp *sdp_h, const st
   }
   const Sdp &s = sdp_of(sdp_h);
   for (int k = 0; k < s.nblocks; ++k)
-    if (s.bn[k] > 118) {
-      set_error("strom_admm_setup: block order > 118 not supported by this K-EIG build");
+    if (s.bn[k] > 112) {
+      set_error("strom_admm_setup: block order > 112 not supported by this K-EIG build");
       return STROM_ENOTIMPL;
     }
   std::unique_ptr<strom_admm> h(new strom_admm);
@@ -749,6 +769,16 @@ strom_status strom_admm_setup(strom_admm **out, const strom_sdp *sdp_h, const st
       else h->eig_class_blocks[it - nps.begin()].push_back(k);
     }
     h->eig_class_np = nps;
+    double best = -1.0;
+    for (size_t c = 0; c < nps.size(); ++c) {
+      const double w = (double)h->eig_class_blocks[c].size() * nps[c] * nps[c] * nps[c];
+      if (w > best) { best = w; h->eig_main_class = (int)c; }
+    }
+    if (nps.size() > 1) {
+      CK(cudaStreamCreateWithFlags(&h->stream2, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&h->fork_ev, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&h->join_ev, cudaEventDisableTiming));
+    }
     for (size_t c = 0; c < nps.size(); ++c) {
       int32_t *pd;
       if ((st = h->upload(pd, h->eig_class_blocks[c]))) return st;

@@ -15,7 +15,7 @@ for r in data[skip:]:
         name += r[ki][r[ki].index('<'):r[ki].index('>') + 1]
     v = float(r[vi].replace(',', ''))
     u = r[ui]
-    us = v / 1000 if u == 'nsecond' else (v if u == 'usecond' else v * 1000)
+    us = {'ns': v / 1000, 'nsecond': v / 1000, 'us': v, 'usecond': v, 'ms': v * 1000, 'msecond': v * 1000}[u]
     agg[name].append(us)
 tot = sum(sum(v) for v in agg.values())
 print(f"{'kernel':32s} {'n':>4s} {'mean us':>9s} {'min us':>8s} {'share':>6s}")
