@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(512, 1) k_eig(EigArgs a) {
   const int64_t off = a.boff[bidx];
   const int L = n * (n + 1) / 2;
   double *U = sm;                 // n columns x n rows, column-major (column j at U + j*n)
-  double *V = sm + n * n;         // same layout
+  double *V = sm + n * n;         // warm-start basis (only until U is formed), same layout
   double *lamv = sm + 2 * n * n;  // n eigenvalues
   unsigned short *sched = (unsigned short *)(lamv + n + 8);  // (p | q << 8) per (round, pair)
   const int tid = threadIdx.x, nt = blockDim.x;
@@ -100,14 +100,15 @@ __global__ void __launch_bounds__(512, 1) k_eig(EigArgs a) {
     if (tid == 0) red[127] = sqrt(v1[0]);
     __syncthreads();
   }
-  const double s = red[127] * (1.0 + 1e-12) + 1e-300;   // s >= ||X_b||_2
+  // shift s = 2 ||X_b||_F >= 2 ||X_b||_2: every column of U = (X_b + sI)V keeps a norm
+  // lambda_j + s >= ||X_b||_F, so v_j = u_j / ||u_j|| is accurate for every j
+  const double s = 2.0 * red[127] + 1e-300;
   const double *Xb = a.Xb_out + off;
   // ---- 2. U = (X_b + s I) V with V = V_prev (warm) or I ----------------------------
   for (int e = tid; e < n * n; e += nt) {   // A (symmetric) into U
     const int j = e / n, i = e - j * n;
     const double v = Xb[svec_pos(i, j)];
     U[e] = (i == j) ? v + (warm ? 0.0 : s) : v * isq2;
-    if (proj && !warm) V[e] = (i == j) ? 1.0 : 0.0;
   }
   if (warm) {
     const double *Vp = a.Vstore + a.voff[bidx];
@@ -216,17 +217,6 @@ __global__ void __launch_bounds__(512, 1) k_eig(EigArgs a) {
             nrm[p] = c2 * al - csn + s2 * be;
             nrm[q] = s2 * al + csn + c2 * be;
           }
-          if (proj) {
-            double *vp = V + p * n, *vq = V + q * n;
-#pragma unroll
-            for (int c = 0; c < EPL; ++c) {
-              const int i = sub + G * c;
-              if (i < n) {
-                const double a0 = vp[i], b0 = vq[i];
-                vp[i] = cs * a0 - sn * b0; vq[i] = sn * a0 + cs * b0;
-              }
-            }
-          }
         }
       }
       __syncthreads();
@@ -239,14 +229,20 @@ __global__ void __launch_bounds__(512, 1) k_eig(EigArgs a) {
     if (!converged) atomicCAS(&a.st->eig_fail, 0, bidx + 1);
     atomicAdd(&a.st->eig_sweeps, (unsigned long long)(sweep + 1));
   }
-  // ---- 4. eigenvalues lambda_j = ||u_j|| - s  (u_j = (lambda_j + s) v_j) ------------------
+  // ---- 4. eigenpairs: lambda_j = ||u_j|| - s, v_j = u_j / ||u_j|| (u_j = (lambda_j + s) v_j) ---
   for (int j = warp; j < n; j += nwarps) {
-    const double *uj = U + j * n;
+    double *uj = U + j * n;
     double nn = 0.0;
     for (int i = lane; i < n; i += 32) nn += uj[i] * uj[i];
     nn = warp_sum(nn);
-    if (lane == 0) lamv[j] = sqrt(nn) - s;
+    const double nr = sqrt(nn);
+    if (lane == 0) lamv[j] = nr - s;
+    if (proj) {
+      const double inv = 1.0 / nr;
+      for (int i = lane; i < n; i += 32) uj[i] *= inv;
+    }
   }
+  V = U;                          // eigenvectors now live in the U buffer
   __syncthreads();
   const double *lam = lamv;
   if (!proj) {
@@ -304,10 +300,12 @@ inline int eig_G(int n) {
   static int force = [] { const char *e = getenv("STROM_EIG_G"); return e ? atoi(e) : 0; }();
   if (force == 8 && n <= 64) return 8;
   if (force == 16 && n > 16) return 16;
+  if (force == 32 && n > 16 && n <= 64) return 32;
   return n <= 16 ? 4 : (n <= 64 ? 8 : 16);
 }
 inline int eig_threads(int n) {
   const int H = (n + (n & 1)) / 2, G = eig_G(n), ppw = 32 / G;
+  if (G == 32) return std::min(512, 32 * H);
   int warps = (H + ppw - 1) / ppw;
   int t = 32 * std::max(warps, 1);
   while (t < 512 && (int64_t)n * n > 16LL * t) t += 32;   // warm-start product capacity

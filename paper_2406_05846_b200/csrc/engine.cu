@@ -89,6 +89,27 @@ __device__ __forceinline__ double warp_dot(const double *__restrict__ a, const d
   return warp_sum((s0 + s1) + (s2 + s3));
 }
 
+// CTA-wide split-K dot (deterministic): all threads of the block cooperate on one row.
+__device__ __forceinline__ double cta_dot(const double *__restrict__ a, const double *__restrict__ x,
+                                          int lo, int hi, double *sh) {
+  const int nt = blockDim.x, tid = threadIdx.x;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  int j = lo + tid;
+  for (; j + 3 * nt < hi; j += 4 * nt) {
+    const double a0 = __ldg(a + j), a1 = __ldg(a + j + nt), a2 = __ldg(a + j + 2 * nt), a3 = __ldg(a + j + 3 * nt);
+    s0 += a0 * x[j]; s1 += a1 * x[j + nt]; s2 += a2 * x[j + 2 * nt]; s3 += a3 * x[j + 3 * nt];
+  }
+  for (; j < hi; j += nt) s0 += __ldg(a + j) * x[j];
+  double v = warp_sum((s0 + s1) + (s2 + s3));
+  const int lane = tid & 31, wid = tid >> 5;
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  double t = (tid < (nt >> 5)) ? sh[tid] : 0.0;
+  if (wid == 0) t = warp_sum(t);
+  __syncthreads();
+  return t;   // valid in warp 0
+}
+
 // ============================ K-TRSV phases ================================
 // P1: u_Q = r_Q - G r_L            (leaf elimination, forward)
 __global__ void k_solve_p1(SolveDev d, RhsArgs ra, const DevState *st) {
@@ -106,11 +127,25 @@ __global__ void k_solve_p1(SolveDev d, RhsArgs ra, const DevState *st) {
 // mode 0: out[R_k + i] = sum_{j<=i} Linv[i][j] in[R_k + j]      (P2: v = L^{-1} u)
 // mode 1: out[R_k + i] = sum_{j>=i} LinvT[i][j] in[R_k + j]     (P6b: y = L^{-T} t)
 struct GemvItem { int32_t uid, row, list, cnt; };
-__global__ void k_gemv_stage(SolveDev d, const GemvItem *items, int nitems, const int32_t *stage_list,
-                             int mode, const double *in, double *out, const DevState *st) {
+// Items with cnt == 1 (a factor used by one stage, e.g. clique 0) come first and get a
+// whole CTA each (split-K); shared factors get one warp per (row, <= 8 stages).
+__global__ void __launch_bounds__(256) k_gemv_stage(SolveDev d, const GemvItem *items, int nitems,
+                                                    int nsingle, const int32_t *stage_list, int mode,
+                                                    const double *in, double *out, const DevState *st) {
   if (st->done) return;
-  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  __shared__ double sh[32];
   const int lane = threadIdx.x & 31;
+  if ((int)blockIdx.x < nsingle) {
+    const GemvItem it = items[blockIdx.x];
+    const int n = d.uid_n[it.uid];
+    const double *M = (mode == 0 ? d.Linv[it.uid] : d.LinvT[it.uid]) + (int64_t)it.row * n;
+    const int jlo = mode == 0 ? 0 : it.row, jhi = mode == 0 ? it.row + 1 : n;
+    const int b0 = d.R_off[stage_list[it.list]];
+    const double sum = cta_dot(M, in + b0, jlo, jhi, sh);
+    if (threadIdx.x == 0) out[b0 + it.row] = sum;
+    return;
+  }
+  const int w = nsingle + (((int)blockIdx.x - nsingle) * (int)blockDim.x + (int)threadIdx.x) / 32;
   if (w >= nitems) return;
   const GemvItem it = items[w];
   const int n = d.uid_n[it.uid];
@@ -122,11 +157,6 @@ __global__ void k_gemv_stage(SolveDev d, const GemvItem *items, int nitems, cons
   for (int c = 0; c < kGemvChunk; ++c) {
     base[c] = c < it.cnt ? d.R_off[stage_list[it.list + c]] : 0;
     acc[c] = 0.0;
-  }
-  if (it.cnt == 1) {   // unique (non-shared) factor: plain unrolled dot
-    const double s = warp_dot(M, in + base[0], jlo, jhi, lane);
-    if (lane == 0) out[base[0] + it.row] = s;
-    return;
   }
   int j = jlo + lane;
   for (; j + 32 < jhi; j += 64) {
@@ -144,56 +174,41 @@ __global__ void k_gemv_stage(SolveDev d, const GemvItem *items, int nitems, cons
 #pragma unroll
   for (int c = 0; c < kGemvChunk; ++c) {
     if (c < it.cnt) {
-      const double s = warp_sum(acc[c]);
-      if (lane == 0) out[base[c] + it.row] = s;
+      const double s2 = warp_sum(acc[c]);
+      if (lane == 0) out[base[c] + it.row] = s2;
     }
   }
 }
 
-// P3: u_S' = u_S - sum_k F_k^T v_k  (warp per separator row, in place on u)
-__global__ void k_solve_p3(SolveDev d, const DevState *st) {
+// P3: u_S' = u_S - sum_k F_k^T v_k  (one CTA per separator row, in place on u)
+__global__ void __launch_bounds__(128) k_solve_p3(SolveDev d, const DevState *st) {
   if (st->done) return;
-  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (w >= d.nS) return;
-  const int s = d.S0 + w;
+  __shared__ double sh[32];
+  const int s = d.S0 + blockIdx.x;
   int j = 0;
   while (j + 1 < d.P - 1 && d.S_off[j + 1] <= s) ++j;   // separator block of s
   const int c = s - d.S_off[j];
-  double acc = 0.0;
-  {  // stage j: its right separator is S_j -> F column wl_j + c
-    const int k = j, uid = d.stage_uid[k], nk = d.uid_n[uid], wk = d.uid_w[uid];
-    const double *Ft = d.Ft[uid] + (int64_t)(d.stage_wl[k] + c) * nk;
-    const double *vk = d.v + d.R_off[k];
-    (void)wk;
-    acc += warp_dot(Ft, vk, 0, nk, lane);
-  }
-  {  // stage j+1: its left separator is S_j -> F column c
-    const int k = j + 1, uid = d.stage_uid[k], nk = d.uid_n[uid];
-    const double *Ft = d.Ft[uid] + (int64_t)c * nk;
-    const double *vk = d.v + d.R_off[k];
-    acc += warp_dot(Ft, vk, 0, nk, lane);
-  }
-  if (lane == 0) d.u[s] -= acc;
+  // stage j: its right separator is S_j -> F column wl_j + c; stage j+1: left -> column c
+  const int u0 = d.stage_uid[j], n0 = d.uid_n[u0];
+  const int u1 = d.stage_uid[j + 1], n1 = d.uid_n[u1];
+  const double a0 = cta_dot(d.Ft[u0] + (int64_t)(d.stage_wl[j] + c) * n0, d.v + d.R_off[j], 0, n0, sh);
+  const double a1 = cta_dot(d.Ft[u1] + (int64_t)c * n1, d.v + d.R_off[j + 1], 0, n1, sh);
+  if (threadIdx.x == 0) d.u[s] -= a0 + a1;
 }
 
-// P4 / P5: dense separator solve with explicit L_T^{-1} (warp per row)
+// P4 / P5: dense separator solve with explicit L_T^{-1} (one CTA per row)
 // mode 0: z = L_T^{-1} u_S ; mode 1: y_S = L_T^{-T} z
-__global__ void k_solve_sep(SolveDev d, int mode, double *y, const DevState *st) {
+__global__ void __launch_bounds__(128) k_solve_sep(SolveDev d, int mode, double *y, const DevState *st) {
   if (st->done) return;
-  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (w >= d.nS) return;
+  __shared__ double sh[32];
+  const int w = blockIdx.x;
   const int n = d.nS;
-  double acc = 0.0;
   if (mode == 0) {
-    const double *M = d.LTinv + (int64_t)w * n;
-    const double *x = d.u + d.S0;
-    acc = warp_dot(M, x, 0, w + 1, lane);
-    if (lane == 0) d.z[d.S0 + w] = acc;
+    const double acc = cta_dot(d.LTinv + (int64_t)w * n, d.u + d.S0, 0, w + 1, sh);
+    if (threadIdx.x == 0) d.z[d.S0 + w] = acc;
   } else {
-    const double *M = d.LTinvT + (int64_t)w * n;
-    const double *x = d.z + d.S0;
-    acc = warp_dot(M, x, w, n, lane);
-    if (lane == 0) y[d.S0 + w] = acc;
+    const double acc = cta_dot(d.LTinvT + (int64_t)w * n, d.z + d.S0, w, n, sh);
+    if (threadIdx.x == 0) y[d.S0 + w] = acc;
   }
 }
 
@@ -366,7 +381,7 @@ struct strom_admm {
   DevState *st = nullptr;
   SolveDev sd{};
   int32_t *row_stage_R = nullptr;
-  GemvItem *items = nullptr; int nitems = 0;
+  GemvItem *items = nullptr; int nitems = 0, nsingle = 0;
   int32_t *stage_list = nullptr;
   std::vector<std::vector<int32_t>> eig_class_blocks;
   std::vector<int32_t *> eig_class_dev;
@@ -437,17 +452,17 @@ strom_status launch_solve(strom_admm *h, const RhsArgs &ra, double *y, int &nl) 
   if (d.nQ > 0) { mark(h, "trsv_p1_leaf_fwd"); k_solve_p1<<<(d.nQ + TB - 1) / TB, TB, 0, s>>>(d, ra, h->st); ++nl; }
   if (h->nitems > 0) {
     mark(h, "trsv_p2_stage_Linv");
-    k_gemv_stage<<<(h->nitems * 32 + TB - 1) / TB, TB, 0, s>>>(d, h->items, h->nitems, h->stage_list, 0,
-                                                               d.u, d.v, h->st);
+    k_gemv_stage<<<h->nsingle + ((h->nitems - h->nsingle) * 32 + TB - 1) / TB, TB, 0, s>>>(
+        d, h->items, h->nitems, h->nsingle, h->stage_list, 0, d.u, d.v, h->st);
     ++nl;
   }
   if (d.nS > 0) {
     mark(h, "trsv_p3_sep_rhs");
-    k_solve_p3<<<(d.nS * 32 + TB - 1) / TB, TB, 0, s>>>(d, h->st); ++nl;
+    k_solve_p3<<<d.nS, 128, 0, s>>>(d, h->st); ++nl;
     mark(h, "trsv_p4_sep_LTinv");
-    k_solve_sep<<<(d.nS * 32 + TB - 1) / TB, TB, 0, s>>>(d, 0, y, h->st); ++nl;
+    k_solve_sep<<<d.nS, 128, 0, s>>>(d, 0, y, h->st); ++nl;
     mark(h, "trsv_p5_sep_LTinvT");
-    k_solve_sep<<<(d.nS * 32 + TB - 1) / TB, TB, 0, s>>>(d, 1, y, h->st); ++nl;
+    k_solve_sep<<<d.nS, 128, 0, s>>>(d, 1, y, h->st); ++nl;
   }
   const int nR = d.S0 - d.nL;
   if (nR > 0) {
@@ -458,8 +473,8 @@ strom_status launch_solve(strom_admm *h, const RhsArgs &ra, double *y, int &nl) 
       CK(cudaMemcpyAsync(d.t + d.nL, d.v + d.nL, sizeof(double) * nR, cudaMemcpyDeviceToDevice, s));
     }
     mark(h, "trsv_p6b_stage_LinvT");
-    k_gemv_stage<<<(h->nitems * 32 + TB - 1) / TB, TB, 0, s>>>(d, h->items, h->nitems, h->stage_list, 1,
-                                                               d.t, y, h->st);
+    k_gemv_stage<<<h->nsingle + ((h->nitems - h->nsingle) * 32 + TB - 1) / TB, TB, 0, s>>>(
+        d, h->items, h->nitems, h->nsingle, h->stage_list, 1, d.t, y, h->st);
     ++nl;
   }
   if (d.nL > 0) { mark(h, "trsv_p7_leaf_bwd"); k_solve_p7<<<(d.nL + TB - 1) / TB, TB, 0, s>>>(d, ra, y, h->st); ++nl; }
@@ -499,6 +514,7 @@ strom_status launch_eig(strom_admm *h, int mode, const double *yv, int &nl) {
     const int G = eig_G(np);
     if (G == 4) k_eig<4, 4><<<a.nblk, threads, smem, s>>>(a);
     else if (G == 8) k_eig<8, 8><<<a.nblk, threads, smem, s>>>(a);
+    else if (G == 32) k_eig<32, 2><<<a.nblk, threads, smem, s>>>(a);
     else k_eig<16, 8><<<a.nblk, threads, smem, s>>>(a);
     ++nl;
   }
@@ -740,7 +756,7 @@ strom_status strom_admm_setup(strom_admm **out, const strom_sdp *sdp_h, const st
   for (int k = 0; k < F.P; ++k)
     for (int q = F.R_off[k]; q < F.R_off[k + 1]; ++q) rsR[q - d.nL] = k;
   std::vector<int32_t> slist;
-  std::vector<GemvItem> items;
+  std::vector<GemvItem> items, multi;
   for (int u = 0; u < nu; ++u) {
     std::vector<int32_t> stg;
     for (int k = 0; k < F.P; ++k) if (F.stage_uid[k] == u && F.R_off[k + 1] > F.R_off[k]) stg.push_back(k);
@@ -748,9 +764,11 @@ strom_status strom_admm_setup(strom_admm **out, const strom_sdp *sdp_h, const st
       const int cnt = (int)std::min<size_t>(kGemvChunk, stg.size() - c0);
       const int li = (int)slist.size();
       for (int c = 0; c < cnt; ++c) slist.push_back(stg[c0 + c]);
-      for (int i = 0; i < un[u]; ++i) items.push_back(GemvItem{u, i, li, cnt});
+      for (int i = 0; i < un[u]; ++i) multi.push_back(GemvItem{u, i, li, cnt});   // warp per row
     }
   }
+  h->nsingle = (int)items.size();
+  items.insert(items.end(), multi.begin(), multi.end());
   h->nitems = (int)items.size();
   if ((st = h->upload(h->row_stage_R, rsR)) || (st = h->upload(h->stage_list, slist))) return st;
   {
@@ -793,6 +811,7 @@ strom_status strom_admm_setup(strom_admm **out, const strom_sdp *sdp_h, const st
       CK(cudaFuncSetAttribute(k_eig<4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)maxsm));
       CK(cudaFuncSetAttribute(k_eig<8, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)maxsm));
       CK(cudaFuncSetAttribute(k_eig<16, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)maxsm));
+      CK(cudaFuncSetAttribute(k_eig<32, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)maxsm));
     }
   }
   // ---- state, AC = A C, norms -------------------------------------------------
