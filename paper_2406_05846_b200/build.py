@@ -49,7 +49,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if verbose:
             sys.stderr.write(r.stderr)
         objs.append(o)
-    cmd = [nvcc, "-shared", "-o", OUT, *objs, *ARCH, "-Xcompiler", "-fopenmp", "-lgomp"]
+    cmd = [nvcc, "-shared", "-o", OUT, *objs, *ARCH, "-Xcompiler", "-fopenmp", "-lgomp",
+           "-lcusolver", "-lcublas"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

@@ -54,6 +54,8 @@ strom_status strom_debug_host_solve(const strom_sdp *sdp, const strom_admm_confi
   strom::Factor f;
   strom_status st = strom::build_factor(sdp->s, cfg->eps_rel, cfg->eps, f);
   if (st != STROM_OK) return st;
+  st = strom::host_factor_dense(f);
+  if (st != STROM_OK) return st;
   strom::host_solve(f, r, y);
   return STROM_OK;
 }

@@ -1,7 +1,7 @@
 // K-EIG: batched PSD-cone projection (Step 2 of Algorithm 1, PAPER.md:467-472;
 // projection Pi(X) = Q max(0, W) Q^T), included by engine.cu.
 //
-// One CTA per PSD block X_beta (order n <= 112), fp64 throughout:
+// One CTA per PSD block X_beta (order n <= 255; n > 112 keeps U in L2-resident global scratch), fp64 throughout:
 //   1. gather X_b = X + sigma (A* y - C) straight from svec (A* fused);
 //   2. one-sided (Hestenes) Jacobi on the shifted matrix B = X_b + s I, s = ||X_b||_F,
 //      so that B is PSD with eigenvalues lambda + s >= 0 kept apart even when X_b has
@@ -21,6 +21,7 @@ struct EigArgs {
   const double *X, *C, *y;
   double *Xb_out, *S_out;
   double *Vstore; const int64_t *voff;     // warm-start eigenbases (n*n per block)
+  double *Ug, *Ag; const int64_t *uoff;    // global scratch for n > 112 (GU variant)
   DevState *st;
   int32_t max_sweeps; double tol;
   int32_t mode;          // 0 projection; 1 eigenvalues of C - A*y (lambda_min only)
@@ -53,7 +54,7 @@ __device__ __forceinline__ int svec_pos(int i, int j) {  // i, j any order
 }
 
 // G lanes own one column pair (rows i = sub + G*c), 32/G pairs per warp.
-template <int G, int EPL>
+template <int G, int EPL, bool GU>
 __global__ void __launch_bounds__(512, 1) k_eig(EigArgs a) {
   if (a.st->done) return;
   extern __shared__ double sm[];
@@ -66,9 +67,16 @@ __global__ void __launch_bounds__(512, 1) k_eig(EigArgs a) {
   const int NP = n + (n & 1), H = NP / 2;
   const int64_t off = a.boff[bidx];
   const int L = n * (n + 1) / 2;
-  double *U = sm;                 // n columns x n rows, column-major (column j at U + j*n)
-  double *V = sm + n * n;         // warm-start basis (only until U is formed), same layout
-  double *lamv = sm + 2 * n * n;  // n eigenvalues
+  // U: n columns x n rows, column-major (column j at U + j*n). Shared memory for
+  // n <= 112 (A staged in U, warm basis in V); L2-resident global scratch above (GU).
+  double *U, *V, *Abuf, *lamv;
+  if (GU) {
+    U = a.Ug + a.uoff[bidx]; Abuf = a.Ag + a.uoff[bidx]; V = a.Vstore + a.voff[bidx];
+    lamv = sm;
+  } else {
+    U = sm; Abuf = sm; V = sm + n * n;
+    lamv = sm + 2 * n * n;
+  }
   unsigned short *sched = (unsigned short *)(lamv + n + 8);  // (p | q << 8) per (round, pair)
   const int tid = threadIdx.x, nt = blockDim.x;
   const int lane = tid & 31, warp = tid >> 5, nwarps = nt >> 5;
@@ -76,7 +84,7 @@ __global__ void __launch_bounds__(512, 1) k_eig(EigArgs a) {
   const double sigma = a.st->sigma;
   const double isq2 = 0.70710678118654752440;
   const bool proj = (a.mode == 0);
-  const bool warm = proj && a.warm_enable && a.st->eig_warm_valid && n * n <= 16 * nt &&
+  const bool warm = proj && a.warm_enable && a.st->eig_warm_valid &&
                     (a.cold_every <= 0 || (a.st->iter % a.cold_every) != 0);
   for (int e = tid; e < (NP - 1) * H; e += nt) {
     const int r = e / H, P = e - r * H;
@@ -105,35 +113,46 @@ __global__ void __launch_bounds__(512, 1) k_eig(EigArgs a) {
   const double s = 2.0 * red[127] + 1e-300;
   const double *Xb = a.Xb_out + off;
   // ---- 2. U = (X_b + s I) V with V = V_prev (warm) or I ----------------------------
-  for (int e = tid; e < n * n; e += nt) {   // A (symmetric) into U
-    const int j = e / n, i = e - j * n;
-    const double v = Xb[svec_pos(i, j)];
-    U[e] = (i == j) ? v + (warm ? 0.0 : s) : v * isq2;
+  {
+    double *stage = warm ? Abuf : U;     // cold: U = A + sI directly
+    for (int e = tid; e < n * n; e += nt) {   // A (symmetric): column-major == row-major
+      const int j = e / n, i = e - j * n;
+      const double v = Xb[svec_pos(i, j)];
+      stage[e] = (i == j) ? v + (warm ? 0.0 : s) : v * isq2;
+    }
   }
   if (warm) {
-    const double *Vp = a.Vstore + a.voff[bidx];
-    for (int e = tid; e < n * n; e += nt) V[e] = Vp[e];
+    if (!GU) {
+      const double *Vp = a.Vstore + a.voff[bidx];
+      for (int e = tid; e < n * n; e += nt) V[e] = Vp[e];
+    }
     __syncthreads();
-    constexpr int KM = 16;             // n*n <= KM * nt is checked at setup
-    double acc[KM];
+    // column j of the new U = A v_j + s v_j; one warp per column, rows lane + 32c.
+    // Without GU the result overwrites v_j in place (each column is read and written
+    // by one warp only), then U := V.
+    double *dst = GU ? U : V;
+    for (int j = warp; j < n; j += nwarps) {
+      const double *vj = V + j * n;
+      double acc[8];
 #pragma unroll
-    for (int k = 0; k < KM; ++k) {
-      const int e = tid + k * nt;
-      acc[k] = 0.0;
-      if (e < n * n) {
-        const int j = e / n, i = e - j * n;   // column j, row i
-        const double *vj = V + j * n;
-        double t = s * vj[i];
-        for (int q = 0; q < n; ++q) t += U[q * n + i] * vj[q];
-        acc[k] = t;
+      for (int c = 0; c < 8; ++c) acc[c] = 0.0;
+      for (int q = 0; q < n; ++q) {
+        const double vq = vj[q];
+        const double *aq = Abuf + q * n;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const int i = lane + 32 * c;
+          if (i < n) acc[c] += aq[i] * vq;
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const int i = lane + 32 * c;
+        if (i < n) dst[j * n + i] = acc[c] + s * vj[i];
       }
     }
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < KM; ++k) {
-      const int e = tid + k * nt;
-      if (e < n * n) U[e] = acc[k];
-    }
+    if (!GU) U = V;
   }
   __syncthreads();
   // ---- 3. one-sided Jacobi sweeps (round-robin pairs) ---------------------------------
@@ -290,13 +309,16 @@ __global__ void __launch_bounds__(512, 1) k_eig(EigArgs a) {
   for (int e = tid; e < n * n; e += nt) Vs[e] = V[e];
 }
 
+inline bool eig_global(int n) { return n > 112; }
 inline size_t eig_smem_bytes(int n) {
   const int NP = n + (n & 1);
-  return sizeof(double) * (2 * (size_t)n * n + n + 8) + sizeof(unsigned short) * (size_t)(NP - 1) * (NP / 2) + 16;
+  const size_t mats = eig_global(n) ? 0 : 2 * (size_t)n * n;
+  return sizeof(double) * (mats + n + 8) + sizeof(unsigned short) * (size_t)(NP - 1) * (NP / 2) + 16;
 }
 
 // lanes per pair and launch shape for a block of order n
 inline int eig_G(int n) {
+  if (eig_global(n)) return 32;
   static int force = [] { const char *e = getenv("STROM_EIG_G"); return e ? atoi(e) : 0; }();
   if (force == 8 && n <= 64) return 8;
   if (force == 16 && n > 16) return 16;

@@ -11,7 +11,9 @@
 //   finalize                      -> eta, sigma policy, done flag
 // Step 1 needs A(X^k) and A(S^k) only, which the previous iteration produced, so
 // Step 1 costs no SpMV.
+#include <cublas_v2.h>
 #include <cuda_runtime.h>
+#include <cusolverDn.h>
 
 #include <algorithm>
 #include <cstdlib>
@@ -395,6 +397,7 @@ struct strom_admm {
   int launches_per_iter = 0;
   double *lam_dev = nullptr;
   double *Vstore = nullptr; int64_t *voff = nullptr;
+  double *Ug = nullptr, *Ag = nullptr; int64_t *uoff = nullptr;
   // per-kernel event instrumentation of one iteration inside the K-graph
   std::vector<cudaEvent_t> prof_ev;
   std::vector<const char *> prof_names;
@@ -426,12 +429,27 @@ struct strom_admm {
   strom_status upload(T *&p, const std::vector<T> &h) {
     strom_status s = alloc(p, h.size());
     if (s != STROM_OK) return s;
-    if (!h.empty()) CK(cudaMemcpy(p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
+    if (!h.empty()) {   // stream-ordered: pageable cudaMemcpy may return before the DMA lands
+      CK(cudaMemcpyAsync(p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, stream));
+      CK(cudaStreamSynchronize(stream));
+    }
     return STROM_OK;
   }
 };
 
 namespace {
+
+// Host<->device copies ordered on the handle's (non-blocking) stream. A plain
+// cudaMemcpy from pageable memory runs on the legacy stream and may return before
+// its DMA completes, so kernels on the handle's stream could read stale data.
+cudaError_t h2d(strom_admm *h, void *dst, const void *src, size_t bytes) {
+  cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, h->stream);
+  return e != cudaSuccess ? e : cudaStreamSynchronize(h->stream);
+}
+cudaError_t d2h(strom_admm *h, void *dst, const void *src, size_t bytes) {
+  cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, h->stream);
+  return e != cudaSuccess ? e : cudaStreamSynchronize(h->stream);
+}
 
 constexpr int kMaxProfEvents = 96;
 
@@ -511,11 +529,13 @@ strom_status launch_eig(strom_admm *h, int mode, const double *yv, int &nl) {
     const size_t smem = eig_smem_bytes(np);
     cudaStream_t s = (fork && c != h->eig_main_class) ? h->stream2 : h->stream;
     if (s == h->stream) mark(h, eig_names[c < 8 ? c : 7]);
+    a.Ug = h->Ug; a.Ag = h->Ag; a.uoff = h->uoff;
     const int G = eig_G(np);
-    if (G == 4) k_eig<4, 4><<<a.nblk, threads, smem, s>>>(a);
-    else if (G == 8) k_eig<8, 8><<<a.nblk, threads, smem, s>>>(a);
-    else if (G == 32) k_eig<32, 2><<<a.nblk, threads, smem, s>>>(a);
-    else k_eig<16, 8><<<a.nblk, threads, smem, s>>>(a);
+    if (eig_global(np)) k_eig<32, 8, true><<<a.nblk, threads, smem, s>>>(a);
+    else if (G == 4) k_eig<4, 4, false><<<a.nblk, threads, smem, s>>>(a);
+    else if (G == 8) k_eig<8, 8, false><<<a.nblk, threads, smem, s>>>(a);
+    else if (G == 32) k_eig<32, 2, false><<<a.nblk, threads, smem, s>>>(a);
+    else k_eig<16, 8, false><<<a.nblk, threads, smem, s>>>(a);
     ++nl;
   }
   if (fork) {
@@ -590,12 +610,12 @@ strom_status reset_state(strom_admm *h) {
   ds.sigma_period = h->cfg.sigma_period; ds.sigma_ratio = h->cfg.sigma_ratio;
   ds.sigma_factor = h->cfg.sigma_factor; ds.sigma_min = h->cfg.sigma_min; ds.sigma_max = h->cfg.sigma_max;
   DevState old{};
-  CK(cudaMemcpy(&old, h->st, sizeof(DevState), cudaMemcpyDeviceToHost));
+  CK(d2h(h, &old, h->st, sizeof(DevState)));
   nb = old.normb; nc = old.normC;
   ds.eig_sweeps = old.eig_sweeps;
   ds.normb = nb; ds.normC = nc;
   ds.sigma_used = ds.sigma;
-  CK(cudaMemcpy(h->st, &ds, sizeof(DevState), cudaMemcpyHostToDevice));
+  CK(h2d(h, h->st, &ds, sizeof(DevState)));
   return STROM_OK;
 }
 
@@ -604,6 +624,178 @@ strom_status recompute_products(strom_admm *h) {
   k_spmv<<<(h->m + TB - 1) / TB, TB, 0, h->stream>>>(h->m, h->Arp, h->Aci, h->Av, h->X, h->AX, nullptr);
   k_spmv<<<(h->m + TB - 1) / TB, TB, 0, h->stream>>>(h->m, h->Arp, h->Aci, h->Av, h->S, h->AS, nullptr);
   CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(h->stream));
+  return STROM_OK;
+}
+
+}  // namespace
+
+// ============================ dense factorisation on the device =================
+// Setup-only (eq:strom:gpu:cholesky "at the beginning and only once"):
+// cuSOLVER potrf + trtri and cuBLAS trmm/syrk on the dedup'd dense blocks.
+// Column-major L^{-1} is, read row-major, exactly L^{-T}; the row-major copies the
+// solve kernels also need are produced by a transpose kernel.
+__global__ void k_transpose(int rows, int cols, const double *in, double *out) {
+  // in: rows x cols row-major -> out: cols x rows row-major
+  __shared__ double tile[32][33];
+  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int r = by + k, c = bx + threadIdx.x;
+    if (r < rows && c < cols) tile[k][threadIdx.x] = in[(int64_t)r * cols + c];
+  }
+  __syncthreads();
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int c = bx + k, r = by + threadIdx.x;
+    if (r < rows && c < cols) out[(int64_t)c * rows + r] = tile[threadIdx.x][k];
+  }
+}
+
+__global__ void k_zero_upper_colmajor(int n, double *A) {
+  // zero the strictly upper triangle of a column-major n x n matrix
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)n * n) return;
+  const int j = (int)(e / n), i = (int)(e - (int64_t)j * n);
+  if (i < j) A[e] = 0.0;
+}
+
+#define CSOL(call)                                                              \
+  do {                                                                          \
+    cusolverStatus_t s_ = (call);                                               \
+    if (s_ != CUSOLVER_STATUS_SUCCESS) {                                        \
+      set_error(std::string("cuSOLVER error ") + std::to_string((int)s_) + " at " #call); \
+      return STROM_ECUDA;                                                       \
+    }                                                                           \
+  } while (0)
+#define CBLAS(call)                                                             \
+  do {                                                                          \
+    cublasStatus_t s_ = (call);                                                 \
+    if (s_ != CUBLAS_STATUS_SUCCESS) {                                          \
+      set_error(std::string("cuBLAS error ") + std::to_string((int)s_) + " at " #call); \
+      return STROM_ECUDA;                                                       \
+    }                                                                           \
+  } while (0)
+
+namespace {
+
+struct SolverHandles {
+  cusolverDnHandle_t sol = nullptr;
+  cublasHandle_t blas = nullptr;
+  cusolverDnParams_t params = nullptr;
+  ~SolverHandles() {
+    if (params) cusolverDnDestroyParams(params);
+    if (sol) cusolverDnDestroy(sol);
+    if (blas) cublasDestroy(blas);
+  }
+};
+
+// in place: A (n x n column-major, symmetric PD) -> L^{-1} (lower, column-major, upper zeroed)
+strom_status chol_inverse(SolverHandles &H, cudaStream_t s, int n, double *A, int *dinfo, const char *what) {
+  size_t wd = 0, wh = 0;
+  CSOL(cusolverDnXpotrf_bufferSize(H.sol, H.params, CUBLAS_FILL_MODE_LOWER, n, CUDA_R_64F, A, n, CUDA_R_64F,
+                                   &wd, &wh));
+  size_t wd2 = 0, wh2 = 0;
+  CSOL(cusolverDnXtrtri_bufferSize(H.sol, CUBLAS_FILL_MODE_LOWER, CUBLAS_DIAG_NON_UNIT, n, CUDA_R_64F, A, n,
+                                   &wd2, &wh2));
+  wd = std::max(wd, wd2); wh = std::max(wh, wh2);
+  void *dw = nullptr;
+  std::vector<char> hw(std::max<size_t>(wh, 1));
+  CK(cudaMalloc(&dw, std::max<size_t>(wd, 8)));
+  int info = 0;
+  cusolverStatus_t r1 = cusolverDnXpotrf(H.sol, H.params, CUBLAS_FILL_MODE_LOWER, n, CUDA_R_64F, A, n, CUDA_R_64F,
+                                         dw, wd, hw.data(), wh, dinfo);
+  cudaError_t e1 = cudaMemcpyAsync(&info, dinfo, sizeof(int), cudaMemcpyDeviceToHost, s);
+  cudaError_t e2 = cudaStreamSynchronize(s);
+  if (r1 != CUSOLVER_STATUS_SUCCESS || e1 != cudaSuccess || e2 != cudaSuccess) {
+    cudaFree(dw);
+    set_error(std::string("potrf failed on ") + what);
+    return STROM_ECUDA;
+  }
+  if (info != 0) {
+    cudaFree(dw);
+    set_error(std::string("strom_admm_setup: non-positive pivot ") + std::to_string(info) + " factoring " + what);
+    return STROM_EFACTOR;
+  }
+  cusolverStatus_t r2 = cusolverDnXtrtri(H.sol, CUBLAS_FILL_MODE_LOWER, CUBLAS_DIAG_NON_UNIT, n, CUDA_R_64F, A, n,
+                                         dw, wd, hw.data(), wh, dinfo);
+  cudaStreamSynchronize(s);
+  cudaFree(dw);
+  if (r2 != CUSOLVER_STATUS_SUCCESS) { set_error(std::string("trtri failed on ") + what); return STROM_ECUDA; }
+  const int64_t nn = (int64_t)n * n;
+  k_zero_upper_colmajor<<<(unsigned)((nn + 255) / 256), 256, 0, s>>>(n, A);
+  CK(cudaGetLastError());
+  return STROM_OK;
+}
+
+strom_status transpose_into(strom_admm *h, int rows, int cols, const double *in, double *&out) {
+  strom_status st = h->alloc(out, (size_t)rows * cols);
+  if (st) return st;
+  dim3 b(32, 8), g((cols + 31) / 32, (rows + 31) / 32);
+  if (rows > 0 && cols > 0) k_transpose<<<g, b, 0, h->stream>>>(rows, cols, in, out);
+  CK(cudaGetLastError());
+  return STROM_OK;
+}
+
+strom_status device_factor_dense(strom_admm *h, std::vector<const double *> &Linv, std::vector<const double *> &LinvT,
+                                 std::vector<const double *> &Fp, std::vector<const double *> &Ftp,
+                                 std::vector<int32_t> &un, std::vector<int32_t> &uw, double *&LTinv, double *&LTinvT) {
+  const Factor &F = h->F;
+  SolverHandles H;
+  CSOL(cusolverDnCreate(&H.sol));
+  CSOL(cusolverDnSetStream(H.sol, h->stream));
+  CSOL(cusolverDnCreateParams(&H.params));
+  CBLAS(cublasCreate(&H.blas));
+  CBLAS(cublasSetStream(H.blas, h->stream));
+  CBLAS(cublasSetMathMode(H.blas, CUBLAS_DEFAULT_MATH));
+  int *dinfo = nullptr;
+  strom_status st = h->alloc(dinfo, 1);
+  if (st) return st;
+  const int nu = (int)F.uK.size();
+  std::vector<double *> Fcm(nu, nullptr);   // column-major F (n_k x w) == row-major F^T
+  for (int u = 0; u < nu; ++u) {
+    const int nk = F.uK[u].rows, w = F.uB[u].cols;
+    un[u] = nk; uw[u] = w;
+    double *A = nullptr;
+    if ((st = h->upload(A, F.uK[u].a))) return st;   // symmetric: row-major == column-major
+    if (nk > 0 && (st = chol_inverse(H, h->stream, nk, A, dinfo, "a stage interior block"))) return st;
+    LinvT[u] = A;                                    // column-major L^{-1} == row-major L^{-T}
+    double *Lr = nullptr;
+    if ((st = transpose_into(h, nk, nk, A, Lr))) return st;
+    Linv[u] = Lr;
+    // F = L^{-1} B : B uploaded column-major (host row-major B transposed)
+    std::vector<double> Bcm((size_t)nk * w);
+    for (int i = 0; i < nk; ++i)
+      for (int c = 0; c < w; ++c) Bcm[(size_t)c * nk + i] = F.uB[u].a[(size_t)i * w + c];
+    double *Bd = nullptr, *Fd = nullptr;
+    if ((st = h->upload(Bd, Bcm)) || (st = h->alloc(Fd, std::max<size_t>((size_t)nk * w, 1)))) return st;
+    if (nk > 0 && w > 0) {
+      const double one = 1.0;
+      CBLAS(cublasDtrmm(H.blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, nk, w,
+                        &one, A, nk, Bd, nk, Fd, nk));
+    }
+    Fcm[u] = Fd;
+    Ftp[u] = Fd;                                     // column-major F == row-major F^T
+    double *Fr = nullptr;
+    if ((st = transpose_into(h, w, nk, Fd, Fr))) return st;   // (w x nk) row-major -> F row-major
+    Fp[u] = Fr;
+  }
+  // separator Schur complement T = K'_SS - sum_k F_k^T F_k, then L_T^{-1}
+  const int nS = F.T0.rows;
+  if (nS > 0) {
+    double *T = nullptr;
+    if ((st = h->upload(T, F.T0.a))) return st;
+    const double one = 1.0, mone = -1.0;
+    for (int k = 0; k < F.P; ++k) {
+      const auto &cm = F.stage_cmap[k];
+      const int u = F.stage_uid[k];
+      if (cm.empty() || un[u] == 0) continue;
+      const int off = cm[0], w = (int)cm.size();
+      CBLAS(cublasDsyrk(H.blas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, w, un[u], &mone, Fcm[u], un[u], &one,
+                        T + (int64_t)off * nS + off, nS));
+    }
+    if ((st = chol_inverse(H, h->stream, nS, T, dinfo, "the separator Schur complement"))) return st;
+    LTinvT = T;
+    if ((st = transpose_into(h, nS, nS, T, LTinv))) return st;
+  }
   CK(cudaStreamSynchronize(h->stream));
   return STROM_OK;
 }
@@ -630,8 +822,8 @@ strom_status strom_admm_setup(strom_admm **out, const strom_sdp *sdp_h, const st
   }
   const Sdp &s = sdp_of(sdp_h);
   for (int k = 0; k < s.nblocks; ++k)
-    if (s.bn[k] > 112) {
-      set_error("strom_admm_setup: block order > 112 not supported by this K-EIG build");
+    if (s.bn[k] > 255) {
+      set_error("strom_admm_setup: block order > 255 not supported by this K-EIG build");
       return STROM_ENOTIMPL;
     }
   std::unique_ptr<strom_admm> h(new strom_admm);
@@ -713,38 +905,18 @@ strom_status strom_admm_setup(strom_admm **out, const strom_sdp *sdp_h, const st
   d.G_ptr = p_Gptr; d.G_col = p_Gcol; d.G_val = p_Gval;
   d.Gt_ptr = p_Gtptr; d.Gt_col = p_Gtcol; d.Gt_val = p_Gtval;
   d.R_off = p_Roff; d.S_off = p_Soff; d.stage_uid = p_suid; d.stage_wl = p_swl; d.stage_wr = p_swr;
-  const int nu = (int)F.Linv.size();
+  // ---- dense factors: computed on the device (setup only) -------------------------
+  const int nu = (int)F.uK.size();
   std::vector<const double *> hLinv(nu), hLinvT(nu), hF(nu), hFt(nu);
   std::vector<int32_t> un(nu), uw(nu);
-  for (int u = 0; u < nu; ++u) {
-    const Dense &Li = F.Linv[u];
-    const Dense &Fu = F.F[u];
-    const int nk = Li.rows, w = Fu.cols;
-    un[u] = nk; uw[u] = w;
-    std::vector<double> LT((size_t)nk * nk), FT((size_t)w * nk);
-    for (int i = 0; i < nk; ++i)
-      for (int j = 0; j < nk; ++j) LT[(size_t)i * nk + j] = Li.a[(size_t)j * nk + i];
-    for (int i = 0; i < nk; ++i)
-      for (int c = 0; c < w; ++c) FT[(size_t)c * nk + i] = Fu.a[(size_t)i * w + c];
-    double *a1, *a2, *a3, *a4;
-    if ((st = h->upload(a1, Li.a)) || (st = h->upload(a2, LT)) || (st = h->upload(a3, Fu.a)) || (st = h->upload(a4, FT)))
-      return st;
-    hLinv[u] = a1; hLinvT[u] = a2; hF[u] = a3; hFt[u] = a4;
-  }
+  double *dLTinv = nullptr, *dLTinvT = nullptr;
+  if ((st = device_factor_dense(h.get(), hLinv, hLinvT, hF, hFt, un, uw, dLTinv, dLTinvT))) return st;
   const double **pp1, **pp2, **pp3, **pp4;
   if ((st = h->upload(pp1, hLinv)) || (st = h->upload(pp2, hLinvT)) || (st = h->upload(pp3, hF)) ||
       (st = h->upload(pp4, hFt)) || (st = h->upload(p_un, un)) || (st = h->upload(p_uw, uw)))
     return st;
   d.Linv = pp1; d.LinvT = pp2; d.F = pp3; d.Ft = pp4; d.uid_n = p_un; d.uid_w = p_uw;
-  if (d.nS > 0) {
-    const int ns = d.nS;
-    std::vector<double> LTT((size_t)ns * ns);
-    for (int i = 0; i < ns; ++i)
-      for (int j = 0; j < ns; ++j) LTT[(size_t)i * ns + j] = F.LTinv.a[(size_t)j * ns + i];
-    double *q1, *q2;
-    if ((st = h->upload(q1, F.LTinv.a)) || (st = h->upload(q2, LTT))) return st;
-    d.LTinv = q1; d.LTinvT = q2;
-  }
+  d.LTinv = dLTinv; d.LTinvT = dLTinvT;
   if ((st = h->alloc(d.u, m)) || (st = h->alloc(d.v, m)) || (st = h->alloc(d.t, m)) || (st = h->alloc(d.z, m)))
     return st;
   CK(cudaMemset(d.u, 0, sizeof(double) * m));
@@ -774,7 +946,7 @@ strom_status strom_admm_setup(strom_admm **out, const strom_sdp *sdp_h, const st
   {
     GemvItem *pi = nullptr;
     if ((st = h->alloc(pi, items.size()))) return st;
-    if (!items.empty()) CK(cudaMemcpy(pi, items.data(), items.size() * sizeof(GemvItem), cudaMemcpyHostToDevice));
+    if (!items.empty()) CK(h2d(h.get(), pi, items.data(), items.size() * sizeof(GemvItem)));
     h->items = pi;
   }
   // ---- eig size classes -----------------------------------------------------
@@ -807,11 +979,18 @@ strom_status strom_admm_setup(strom_admm **out, const strom_sdp *sdp_h, const st
     std::vector<int64_t> voff(s.nblocks + 1, 0);
     for (int k = 0; k < s.nblocks; ++k) voff[k + 1] = voff[k] + (int64_t)s.bn[k] * s.bn[k];
     if ((st = h->upload(h->voff, voff)) || (st = h->alloc(h->Vstore, voff[s.nblocks]))) return st;
+    std::vector<int64_t> uoff(s.nblocks + 1, 0);   // global Jacobi scratch for large blocks
+    for (int k = 0; k < s.nblocks; ++k)
+      uoff[k + 1] = uoff[k] + (eig_global(s.bn[k] + (s.bn[k] & 1)) ? (int64_t)s.bn[k] * s.bn[k] : 0);
+    if ((st = h->upload(h->uoff, uoff)) || (st = h->alloc(h->Ug, uoff[s.nblocks])) ||
+        (st = h->alloc(h->Ag, uoff[s.nblocks])))
+      return st;
     if (maxsm > 48 * 1024) {
-      CK(cudaFuncSetAttribute(k_eig<4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)maxsm));
-      CK(cudaFuncSetAttribute(k_eig<8, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)maxsm));
-      CK(cudaFuncSetAttribute(k_eig<16, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)maxsm));
-      CK(cudaFuncSetAttribute(k_eig<32, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)maxsm));
+      CK(cudaFuncSetAttribute(k_eig<4, 4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)maxsm));
+      CK(cudaFuncSetAttribute(k_eig<8, 8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)maxsm));
+      CK(cudaFuncSetAttribute(k_eig<16, 8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)maxsm));
+      CK(cudaFuncSetAttribute(k_eig<32, 2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)maxsm));
+      CK(cudaFuncSetAttribute(k_eig<32, 8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)maxsm));
     }
   }
   // ---- state, AC = A C, norms -------------------------------------------------
@@ -821,7 +1000,7 @@ strom_status strom_admm_setup(strom_admm **out, const strom_sdp *sdp_h, const st
     for (double v : s.b) nb += v * v;
     for (double v : s.C) nc += v * v;
     ds.normb = std::sqrt(nb); ds.normC = std::sqrt(nc);
-    CK(cudaMemcpy(h->st, &ds, sizeof(DevState), cudaMemcpyHostToDevice));
+    CK(h2d(h.get(), h->st, &ds, sizeof(DevState)));
   }
   if ((st = reset_state(h.get()))) return st;
   k_spmv<<<(m + TB - 1) / TB, TB, 0, h->stream>>>(m, h->Arp, h->Aci, h->Av, h->C, h->AC, nullptr);
@@ -891,7 +1070,7 @@ strom_status strom_admm_solve(strom_admm *h, double tol, int64_t maxiter, int64_
   if (!h || maxiter < 0 || !(tol >= 0.0)) { set_error("strom_admm_solve: bad arguments"); return STROM_EINVAL; }
   CK(cudaSetDevice(h->device));
   DevState ds;
-  CK(cudaMemcpy(&ds, h->st, sizeof(DevState), cudaMemcpyDeviceToHost));
+  CK(d2h(h, &ds, h->st, sizeof(DevState)));
   const int64_t it0 = ds.iter;
   const int32_t zero = 0;
   strom_status st = set_tol(h, tol);
@@ -917,11 +1096,11 @@ strom_status strom_admm_get(strom_admm *h, double *X, double *y, double *S, stro
   if (y) k_permute<<<(h->m + 255) / 256, 256, 0, h->stream>>>(h->m, h->perm, h->y, h->tmp_m, 1);
   CK(cudaStreamSynchronize(h->stream));
   CK(cudaGetLastError());
-  if (X) CK(cudaMemcpy(X, h->X, sizeof(double) * h->n, cudaMemcpyDeviceToHost));
-  if (S) CK(cudaMemcpy(S, h->S, sizeof(double) * h->n, cudaMemcpyDeviceToHost));
-  if (y) CK(cudaMemcpy(y, h->tmp_m, sizeof(double) * h->m, cudaMemcpyDeviceToHost));
+  if (X) CK(d2h(h, X, h->X, sizeof(double) * h->n));
+  if (S) CK(d2h(h, S, h->S, sizeof(double) * h->n));
+  if (y) CK(d2h(h, y, h->tmp_m, sizeof(double) * h->m));
   DevState ds;
-  CK(cudaMemcpy(&ds, h->st, sizeof(DevState), cudaMemcpyDeviceToHost));
+  CK(d2h(h, &ds, h->st, sizeof(DevState)));
   if (res) {
     res->iter = ds.iter; res->eta_p = ds.eta_p; res->eta_d = ds.eta_d; res->eta_g = ds.eta_g;
     res->pobj = ds.pobj; res->dobj = ds.dobj; res->sigma = ds.sigma_used; res->eta_x = ds.eta_x;
@@ -954,9 +1133,9 @@ strom_status strom_admm_lower_bound(strom_admm *h, const double *R_beta, double 
   if (st) return st;
   std::vector<double> lam(h->nblocks), yh(h->m), bh(h->m);
   CK(cudaStreamSynchronize(h->stream));
-  CK(cudaMemcpy(lam.data(), h->lam_dev, sizeof(double) * h->nblocks, cudaMemcpyDeviceToHost));
-  CK(cudaMemcpy(yh.data(), h->y, sizeof(double) * h->m, cudaMemcpyDeviceToHost));
-  CK(cudaMemcpy(bh.data(), h->b, sizeof(double) * h->m, cudaMemcpyDeviceToHost));
+  CK(d2h(h, lam.data(), h->lam_dev, sizeof(double) * h->nblocks));
+  CK(d2h(h, yh.data(), h->y, sizeof(double) * h->m));
+  CK(d2h(h, bh.data(), h->b, sizeof(double) * h->m));
   // <b,y> + sum_beta R_beta min(0, lambda_min); the eigenvalue
   // backward-error floor n*u*||Z|| keeps the bound valid under rounding.
   double by = 0.0;
@@ -993,7 +1172,7 @@ strom_status strom_admm_factor_info(const strom_admm *h, int64_t *device_bytes, 
   if (device_bytes) *device_bytes = h->dev_bytes;
   if (n_leaf_rows) *n_leaf_rows = h->F.nL;
   if (n_sep_rows) *n_sep_rows = h->sd.nS;
-  if (n_unique_dense) *n_unique_dense = (int32_t)h->F.Linv.size();
+  if (n_unique_dense) *n_unique_dense = (int32_t)h->F.uK.size();
   return STROM_OK;
 }
 
@@ -1015,27 +1194,27 @@ strom_status strom_debug_project_psd(strom_admm *h, const double *Xb, double sig
   CK(cudaMemcpyAsync(h->tmp_m, Xb, sizeof(double) * h->n, cudaMemcpyHostToDevice, h->stream));
   CK(cudaMemsetAsync(h->tmp_m2, 0, sizeof(double) * h->n, h->stream));
   DevState ds;
-  CK(cudaMemcpy(&ds, h->st, sizeof(DevState), cudaMemcpyDeviceToHost));
+  CK(d2h(h, &ds, h->st, sizeof(DevState)));
   const double sg_old = ds.sigma;
   const int32_t done_old = ds.done;
   const int32_t warm_old = ds.eig_warm_valid;
   ds.sigma = sigma; ds.done = 0; ds.eig_warm_valid = 0;
-  CK(cudaMemcpy(h->st, &ds, sizeof(DevState), cudaMemcpyHostToDevice));
+  CK(h2d(h, h->st, &ds, sizeof(DevState)));
   h->X = h->tmp_m; h->C = h->tmp_m2;
   int nl = 0;
   strom_status st = launch_eig(h, 0, h->zeros_m, nl);
   h->X = Xsave; h->C = Csave; (void)ysave;
   if (st) return st;
   CK(cudaStreamSynchronize(h->stream));
-  CK(cudaMemcpy(S_out, h->S, sizeof(double) * h->n, cudaMemcpyDeviceToHost));
+  CK(d2h(h, S_out, h->S, sizeof(double) * h->n));
   if (Pi_out) {
     std::vector<double> xb(Xb, Xb + h->n);
     for (int64_t j = 0; j < h->n; ++j) Pi_out[j] = xb[j] + sigma * S_out[j];
   }
-  CK(cudaMemcpy(&ds, h->st, sizeof(DevState), cudaMemcpyDeviceToHost));
+  CK(d2h(h, &ds, h->st, sizeof(DevState)));
   const int32_t fail = ds.eig_fail;
   ds.sigma = sg_old; ds.done = done_old; ds.eig_fail = 0; ds.eig_warm_valid = warm_old;
-  CK(cudaMemcpy(h->st, &ds, sizeof(DevState), cudaMemcpyHostToDevice));
+  CK(h2d(h, h->st, &ds, sizeof(DevState)));
   // restore S of the iterate is not needed for tests (they reset with set_start)
   if (fail) { set_error("Jacobi sweep cap reached"); return STROM_EEIG; }
   return STROM_OK;
@@ -1046,24 +1225,24 @@ strom_status strom_debug_spmv(strom_admm *h, const double *X, double *AX, const 
   CK(cudaSetDevice(h->device));
   const int TB = 256;
   if (X && AX) {
-    CK(cudaMemcpy(h->tmp_m2, X, sizeof(double) * h->n, cudaMemcpyHostToDevice));
+    CK(h2d(h, h->tmp_m2, X, sizeof(double) * h->n));
     k_spmv<<<(h->m + TB - 1) / TB, TB, 0, h->stream>>>(h->m, h->Arp, h->Aci, h->Av, h->tmp_m2, h->tmp_m, nullptr);
     k_permute<<<(h->m + TB - 1) / TB, TB, 0, h->stream>>>(h->m, h->perm, h->tmp_m, h->tmp_m2, 1);
     CK(cudaStreamSynchronize(h->stream));
-    CK(cudaMemcpy(AX, h->tmp_m2, sizeof(double) * h->m, cudaMemcpyDeviceToHost));
+    CK(d2h(h, AX, h->tmp_m2, sizeof(double) * h->m));
   }
   if (y && Aty) {
     // A* y = X_b of the eig gather with X = 0, C = 0, sigma = 1 would need eig; use a
     // dedicated column gather via k_update-like loop on the host-visible path:
     std::vector<double> yi(h->m);
     for (int i = 0; i < h->m; ++i) yi[i] = y[h->F.perm[i]];
-    CK(cudaMemcpy(h->tmp_m, yi.data(), sizeof(double) * h->m, cudaMemcpyHostToDevice));
+    CK(h2d(h, h->tmp_m, yi.data(), sizeof(double) * h->m));
     // reuse k_spmv on A^T (column CSR)
     k_spmv<<<(int)((h->n + TB - 1) / TB), TB, 0, h->stream>>>((int)h->n, h->Atp, h->Atr, h->Atv, h->tmp_m,
                                                               h->tmp_m2, nullptr);
     CK(cudaStreamSynchronize(h->stream));
     CK(cudaGetLastError());
-    CK(cudaMemcpy(Aty, h->tmp_m2, sizeof(double) * h->n, cudaMemcpyDeviceToHost));
+    CK(d2h(h, Aty, h->tmp_m2, sizeof(double) * h->n));
   }
   return STROM_OK;
 }
@@ -1073,13 +1252,13 @@ strom_status strom_debug_solve(strom_admm *h, const double *r, double *y) {
   CK(cudaSetDevice(h->device));
   std::vector<double> ri(h->m);
   for (int i = 0; i < h->m; ++i) ri[i] = r[h->F.perm[i]];
-  CK(cudaMemcpy(h->tmp_m, ri.data(), sizeof(double) * h->m, cudaMemcpyHostToDevice));
+  CK(h2d(h, h->tmp_m, ri.data(), sizeof(double) * h->m));
   DevState ds;
-  CK(cudaMemcpy(&ds, h->st, sizeof(DevState), cudaMemcpyDeviceToHost));
+  CK(d2h(h, &ds, h->st, sizeof(DevState)));
   const double sg = ds.sigma;
   const int32_t dn = ds.done;
   ds.sigma = 1.0; ds.done = 0;
-  CK(cudaMemcpy(h->st, &ds, sizeof(DevState), cudaMemcpyHostToDevice));
+  CK(h2d(h, h->st, &ds, sizeof(DevState)));
   RhsArgs ra{h->tmp_m, h->zeros_m, h->zeros_m, h->zeros_m};
   int nl = 0;
   strom_status st = launch_solve(h, ra, h->tmp_m2, nl);
@@ -1087,9 +1266,9 @@ strom_status strom_debug_solve(strom_admm *h, const double *r, double *y) {
   k_permute<<<(h->m + 255) / 256, 256, 0, h->stream>>>(h->m, h->perm, h->tmp_m2, h->tmp_m, 1);
   CK(cudaStreamSynchronize(h->stream));
   CK(cudaGetLastError());
-  CK(cudaMemcpy(y, h->tmp_m, sizeof(double) * h->m, cudaMemcpyDeviceToHost));
+  CK(d2h(h, y, h->tmp_m, sizeof(double) * h->m));
   ds.sigma = sg; ds.done = dn;
-  CK(cudaMemcpy(h->st, &ds, sizeof(DevState), cudaMemcpyHostToDevice));
+  CK(h2d(h, h->st, &ds, sizeof(DevState)));
   return STROM_OK;
 }
 

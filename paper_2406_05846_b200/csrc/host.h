@@ -53,7 +53,12 @@ struct Factor {
   // stage interiors R_k = [R_off[k], R_off[k+1]) ; separators S_j = [S_off[j], S_off[j+1])
   std::vector<int32_t> R_off;  // P + 1
   std::vector<int32_t> S_off;  // P (S_0 .. S_{P-2}); S_off[0] = R_off[P]
-  // unique dense stage factors
+  // unique dense stage blocks (inputs of the dense backend)
+  std::vector<Dense> uK;       // K'_{R_k R_k}
+  std::vector<Dense> uB;       // K'_{R_k, [S_{k-1} S_k]}
+  Dense T0;                    // K'_SS
+  std::vector<std::vector<int32_t>> stage_cmap;
+  // unique dense stage factors (host backend output)
   std::vector<Dense> Linv;     // lower-triangular L_k^{-1} (n_k x n_k)
   std::vector<Dense> F;        // L_k^{-1} K'_{R_k, [S_{k-1} S_k]}  (n_k x (wl + wr))
   std::vector<int32_t> stage_uid;       // stage -> unique factor id
@@ -65,6 +70,7 @@ struct Factor {
 strom_status build_sdp(Sdp &s, int32_t nblocks, const strom_block *blocks, int32_t m,
                        const double *b);
 strom_status build_factor(const Sdp &s, double eps_rel, double eps_abs, Factor &f);
+strom_status host_factor_dense(Factor &f);
 // Host execution of the factored solve (test hook / reference for the device phases).
 void host_solve(const Factor &f, const double *r_orig, double *y_orig);
 

@@ -256,8 +256,16 @@ strom_status build_factor(const Sdp &s, double eps_rel, double eps_abs, Factor &
     }
     owner[i] = lo;
     is_sep[i] = (hi == lo + 1);
+  }
+  // A leaf candidate is a two-term row inside one block that owns a private column
+  // (referenced by no other row) -- the non-canonical occurrence of an A_mom row
+  // (PAPER.md:344). Groups then form only through the shared canonical column.
+  std::vector<int32_t> col_count(s.n, 0);
+  for (int64_t t = 0; t < (int64_t)s.col.size(); ++t) col_count[s.col[t]]++;
+  for (int i = 0; i < m; ++i) {
     const int64_t a = s.rowptr[i];
-    if (!is_sep[i] && s.rowptr[i + 1] - a == 2 && col_block[s.col[a]] == col_block[s.col[a + 1]])
+    if (!is_sep[i] && s.rowptr[i + 1] - a == 2 && col_block[s.col[a]] == col_block[s.col[a + 1]] &&
+        (col_count[s.col[a]] == 1 || col_count[s.col[a + 1]] == 1))
       leaf_cand[i] = 1;
   }
   // ---- K = AA* + eps I ----------------------------------------------------
@@ -459,38 +467,48 @@ strom_status build_factor(const Sdp &s, double eps_rel, double eps_abs, Factor &
         found = (int)u; break;
       }
     if (found >= 0) { f.stage_uid[k] = found; continue; }
-    // new unique factor
-    Dense L = Kd;
-    if (nk > 0 && !dense_cholesky_lower(L)) {
-      set_error("strom_admm_setup: non-positive pivot in stage " + std::to_string(k) + " interior block");
-      return STROM_EFACTOR;
-    }
-    Dense Li; dense_trinv_lower(L, Li);
-    Dense Fk; dense_gemm_lowertri(Li, Bd, Fk);
-    f.stage_uid[k] = (int)f.Linv.size();
-    f.Linv.push_back(std::move(Li));
-    f.F.push_back(std::move(Fk));
+    f.stage_uid[k] = (int)f.uK.size();
+    f.uK.push_back(Kd); f.uB.push_back(Bd);
     uid_hash.push_back(h); uid_K.push_back(std::move(Kd)); uid_B.push_back(std::move(Bd));
   }
-  // ---- separator Schur complement T ---------------------------------------------
-  Dense T; T.rows = T.cols = nS; T.a.assign((size_t)nS * nS, 0.0);
+  f.stage_cmap = stage_cmap;
+  // ---- separator block K'_SS (its Schur complement T is formed by the backend) -----
+  f.T0.rows = f.T0.cols = nS; f.T0.a.assign((size_t)nS * nS, 0.0);
   for (int si = 0; si < nS; ++si) {
     const int qi = S0 + si - nL;
     for (size_t t = 0; t < KPi[qi].size(); ++t) {
       const int qj = KPi[qi][t] + nL;
-      if (qj >= S0) T.row(si)[qj - S0] = KPv[qi][t];
+      if (qj >= S0) f.T0.row(si)[qj - S0] = KPv[qi][t];
     }
   }
-  for (int k = 0; k < P; ++k)
-    if (!stage_cmap[k].empty() && f.R_off[k + 1] > f.R_off[k])
-      dense_sub_AtA(T, f.F[f.stage_uid[k]], stage_cmap[k]);
-  if (nS > 0) {
-    Dense LT = T;
-    if (!dense_cholesky_lower(LT)) {
+  return STROM_OK;
+}
+
+// Host backend of the dense factorisation (tests and small problems):
+// L_u = chol(K'_u), L_u^{-1}, F_u = L_u^{-1} B_u; T = K'_SS - sum F^T F, L_T^{-1}.
+strom_status host_factor_dense(Factor &f) {
+  f.Linv.clear(); f.F.clear();
+  for (size_t u = 0; u < f.uK.size(); ++u) {
+    Dense L = f.uK[u];
+    if (L.rows > 0 && !dense_cholesky_lower(L)) {
+      set_error("strom_admm_setup: non-positive pivot in a stage interior block");
+      return STROM_EFACTOR;
+    }
+    Dense Li; dense_trinv_lower(L, Li);
+    Dense Fk; dense_gemm_lowertri(Li, f.uB[u], Fk);
+    f.Linv.push_back(std::move(Li));
+    f.F.push_back(std::move(Fk));
+  }
+  Dense T = f.T0;
+  for (int k = 0; k < f.P; ++k)
+    if (!f.stage_cmap[k].empty() && f.R_off[k + 1] > f.R_off[k])
+      dense_sub_AtA(T, f.F[f.stage_uid[k]], f.stage_cmap[k]);
+  if (T.rows > 0) {
+    if (!dense_cholesky_lower(T)) {
       set_error("strom_admm_setup: non-positive pivot in the separator Schur complement");
       return STROM_EFACTOR;
     }
-    dense_trinv_lower(LT, f.LTinv);
+    dense_trinv_lower(T, f.LTinv);
   }
   return STROM_OK;
 }

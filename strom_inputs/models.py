@@ -165,6 +165,9 @@ SYNTH_SHAPES = {
     "landing": (8, 2, 10),     # |I| = 18 -> 190 / 19 (PAPER.md:704, 499 at N=50)
     "flying": (8, 4, 11),      # |I| = 20 -> 231 / 21 (PAPER.md:706, 659 at N=60)
     "small": (2, 1, 2),        # |I| = 5 -> 21 / 6, fast parity case
+    "wide190": (2, 14, 2),     # |I| = 18 -> 190 / 19 blocks, few rows: parity of large K-EIG
+    "wide231": (2, 16, 2),     # |I| = 20 -> 231 / 21 blocks
+    "cartpole": (5, 3, 9),     # |I| = 13 -> 105 / 14 (273 localizing at N=30)
 }
 
 

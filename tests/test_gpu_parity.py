@@ -1,7 +1,7 @@
 """GPU parity: the CUDA path (through the C-ABI) against the oracle, element by
 element on the same seeded inputs (SURVEY.md §8(c) parity contract).
 
-Tolerances: single kernels 1e-12 relative (projection),
+Tolerances: single kernels max(1e-12, 5e-14 n) relative (projection),
 1e-13 (SpMV), 1e-10 on range quantities of the solve (A*y; y itself is
 eps-amplified off range(A), F2/Q26); 50 iterations of Algorithm 1: 1e-9
 relative on X, S, A*y and <b, y> (north_star).
@@ -34,7 +34,10 @@ def case(name):
                "pend3": lambda: models.pendulum(3, 1.2, -3.0),
                "pend30": lambda: models.pendulum(30, 0.1, 0.0),
                "synth": lambda: models.synthetic_shape("small", 6, seed=1),
-               "toy": lambda: models.toy(4)}[name]()
+               "toy": lambda: models.toy(4),
+               "wide190": lambda: models.synthetic_shape("wide190", 2, seed=2),
+               "wide231": lambda: models.synthetic_shape("wide231", 2, seed=3),
+               "cartpole": lambda: models.synthetic_shape("cartpole", 3, seed=4)}[name]()
         _CACHE[name] = compile_relaxation(pop)
     return _CACHE[name]
 
@@ -45,7 +48,7 @@ def make(sdp, **cfg):
 
 
 # ---------------------------------------------------------------- kernels
-@pytest.mark.parametrize("name", ["pend5", "synth", "toy"])
+@pytest.mark.parametrize("name", ["pend5", "synth", "toy", "cartpole", "wide190", "wide231"])
 def test_projection_parity(name):
     sdp = case(name)
     g = make(sdp)
@@ -58,7 +61,10 @@ def test_projection_parity(name):
         bo = sdp.block_offset
         for beta in range(sdp.nblocks):
             sl = slice(bo[beta], bo[beta + 1])
-            assert rel(S_gpu[sl], S_ref[sl]) <= 1e-12, (beta, rel(S_gpu[sl], S_ref[sl]))
+            # eigensolver backward error O(n u s), s = 2||X_b||_F the Jacobi shift: 5e-14 n
+            # (DESIGN.md §7); the 1e-9 contract is on iterates, tested below
+            tol = max(1e-12, 5e-14 * int(sdp.block_n[beta]))
+            assert rel(S_gpu[sl], S_ref[sl]) <= tol, (beta, rel(S_gpu[sl], S_ref[sl]))
 
 
 def test_projection_edge_cases():
@@ -218,3 +224,17 @@ def test_single_stage_no_separators():
     o = Oracle(sdp)
     g.iterate(20); o.iterate(20)
     _compare(g, o, 1e-9, "single-stage")
+
+
+@pytest.mark.parametrize("name", ["cartpole", "wide190", "wide231"])
+def test_large_block_iterations_parity(name):
+    """Block orders 105 (cart-pole), 190 (car back-in / landing,
+    PAPER.md:702-704) and 231 (flying robot): shared-memory and
+    global-scratch K-EIG variants plus the device-side dense factorisation."""
+    sdp = case(name)
+    g = make(sdp, check_every=5)
+    o = Oracle(sdp)
+    g.iterate(5); o.iterate(5)
+    _compare(g, o, 1e-9, f"{name}@5")
+    g.iterate(15); o.iterate(15)
+    _compare(g, o, 1e-9, f"{name}@20")
