@@ -50,7 +50,7 @@ def extract_zbar(sdp, X: np.ndarray) -> np.ndarray:
     return acc / np.maximum(cnt, 1)
 
 
-def pendulum_upper_bound(sdp, X: np.ndarray, maxiter: int = 200):
+def pendulum_upper_bound(sdp, X: np.ndarray, maxiter: int = 200, u_start=None):
     """p_hat for the pendulum POP: controls of z_bar, then a local solve over the
     controls (rollouts satisfy x_0 = x_init, the dynamics and SO(2) exactly;
     |u| <= 1 and fc_k >= fc_min are the local solver's constraints)."""
@@ -63,6 +63,9 @@ def pendulum_upper_bound(sdp, X: np.ndarray, maxiter: int = 200):
     th0, thd0 = pop.meta["theta0"], pop.meta["theta_dot0"]
     zbar = extract_zbar(sdp, X)
     u0 = np.clip(np.array([zbar[5 * k + 4] for k in range(N)]), -1.0, 1.0)
+    if u_start is not None:   # keep the better of the extracted and the previous controls
+        if pop.objective(pendulum_rollout(N, u_start, th0, thd0, p)) < pop.objective(pendulum_rollout(N, u0, th0, thd0, p)):
+            u0 = np.asarray(u_start, dtype=np.float64)
 
     def rollout(u):
         return pendulum_rollout(N, u, th0, thd0, p)
@@ -81,6 +84,10 @@ def pendulum_upper_bound(sdp, X: np.ndarray, maxiter: int = 200):
     z_hat = rollout(u)
     feasible = bool(np.all(margin(u) >= -1e-9))
     return pop.objective(z_hat), z_hat, feasible
+
+
+def pendulum_controls(z_hat: np.ndarray, N: int) -> np.ndarray:
+    return np.array([z_hat[5 * k + 4] for k in range(N)])
 
 
 def suboptimality_gap(p_hat: float, lb: float) -> float:
