@@ -182,7 +182,8 @@ __global__ void __launch_bounds__(256) k_gemv_stage(SolveDev d, const GemvItem *
   }
 }
 
-// P3: u_S' = u_S - sum_k F_k^T v_k  (one CTA per separator row, in place on u)
+// P3: u_S -= sum_k F_k^T v_k = sum_k H_k^T u_Rk  (H_k = L_k^{-T} F_k, so it needs only P1's
+// output and runs concurrently with P2; one CTA per separator row, in place on u)
 __global__ void __launch_bounds__(128) k_solve_p3(SolveDev d, const DevState *st) {
   if (st->done) return;
   __shared__ double sh[32];
@@ -190,11 +191,11 @@ __global__ void __launch_bounds__(128) k_solve_p3(SolveDev d, const DevState *st
   int j = 0;
   while (j + 1 < d.P - 1 && d.S_off[j + 1] <= s) ++j;   // separator block of s
   const int c = s - d.S_off[j];
-  // stage j: its right separator is S_j -> F column wl_j + c; stage j+1: left -> column c
+  // stage j: its right separator is S_j -> column wl_j + c; stage j+1: left -> column c
   const int u0 = d.stage_uid[j], n0 = d.uid_n[u0];
   const int u1 = d.stage_uid[j + 1], n1 = d.uid_n[u1];
-  const double a0 = cta_dot(d.Ft[u0] + (int64_t)(d.stage_wl[j] + c) * n0, d.v + d.R_off[j], 0, n0, sh);
-  const double a1 = cta_dot(d.Ft[u1] + (int64_t)c * n1, d.v + d.R_off[j + 1], 0, n1, sh);
+  const double a0 = cta_dot(d.Ht[u0] + (int64_t)(d.stage_wl[j] + c) * n0, d.u + d.R_off[j], 0, n0, sh);
+  const double a1 = cta_dot(d.Ht[u1] + (int64_t)c * n1, d.u + d.R_off[j + 1], 0, n1, sh);
   if (threadIdx.x == 0) d.u[s] -= a0 + a1;
 }
 
@@ -214,8 +215,9 @@ __global__ void __launch_bounds__(128) k_solve_sep(SolveDev d, int mode, double 
   }
 }
 
-// P6a: t_Rk = v_Rk - F_k y_S,adj   (warp per interior row)
-__global__ void k_solve_p6a(SolveDev d, const int32_t *row_stage, const double *y, const DevState *st) {
+// P6'': y_Rk = w_Rk - H_k y_S,adj with w = L_k^{-T} L_k^{-1} u (P6'), H_k = L_k^{-T} F_k
+// (warp per interior row)
+__global__ void k_solve_p6a(SolveDev d, const int32_t *row_stage, double *y, const DevState *st) {
   if (st->done) return;
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   const int nR = d.S0 - d.nL;
@@ -224,14 +226,14 @@ __global__ void k_solve_p6a(SolveDev d, const int32_t *row_stage, const double *
   const int k = row_stage[w];
   const int uid = d.stage_uid[k], wk = d.uid_w[uid], wl = d.stage_wl[k];
   const int i = q - d.R_off[k];
-  const double *Fi = d.F[uid] + (int64_t)i * wk;
+  const double *Hi = d.H[uid] + (int64_t)i * wk;
   double acc = 0.0;
   for (int c = lane; c < wk; c += 32) {
     const int s = c < wl ? d.S_off[k - 1] + c : d.S_off[k] + (c - wl);
-    acc += __ldg(Fi + c) * y[s];
+    acc += __ldg(Hi + c) * y[s];
   }
   acc = warp_sum(acc);
-  if (lane == 0) d.t[q] = d.v[q] - acc;
+  if (lane == 0) y[q] = d.t[q] - acc;
 }
 
 // P7: y_L = K_LL^{-1} r_L - G^T y_Q   (thread per leaf row)
@@ -390,7 +392,7 @@ struct strom_admm {
   std::vector<int> eig_class_np;
   int eig_main_class = 0;                    // class with the largest n^3 work
   cudaStream_t stream2 = nullptr;            // fork for concurrent eig size classes
-  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr, sfork_ev = nullptr, sjoin_ev = nullptr;
   cudaGraph_t graphK = nullptr, graph1 = nullptr;
   cudaGraphExec_t execK = nullptr, exec1 = nullptr;
   int K = 50;
@@ -406,6 +408,8 @@ struct strom_admm {
   ~strom_admm() {
     for (cudaEvent_t e : prof_ev) cudaEventDestroy(e);
     if (fork_ev) cudaEventDestroy(fork_ev);
+    if (sfork_ev) cudaEventDestroy(sfork_ev);
+    if (sjoin_ev) cudaEventDestroy(sjoin_ev);
     if (join_ev) cudaEventDestroy(join_ev);
     if (stream2) cudaStreamDestroy(stream2);
     if (execK) cudaGraphExecDestroy(execK);
@@ -463,43 +467,46 @@ void mark(strom_admm *h, const char *name) {
 }
 
 strom_status launch_solve(strom_admm *h, const RhsArgs &ra, double *y, int &nl) {
+  // P1 -> { main: P2 (v = L^{-1} u), P6' (w = L^{-T} v) | fork: P3 (u_S -= H^T u_R), P4, P5 }
+  //    -> join -> P6'' (y_R = w - H y_S) -> P7. Critical path 6 kernels.
   const SolveDev &d = h->sd;
   cudaStream_t s = h->stream;
   const int TB = 256;
   nl = 0;
+  const int nR = d.S0 - d.nL;
   if (d.nQ > 0) { mark(h, "trsv_p1_leaf_fwd"); k_solve_p1<<<(d.nQ + TB - 1) / TB, TB, 0, s>>>(d, ra, h->st); ++nl; }
-  if (h->nitems > 0) {
+  const bool fork = d.nS > 0 && h->stream2;
+  if (fork) {
+    CK(cudaEventRecord(h->sfork_ev, s));
+    CK(cudaStreamWaitEvent(h->stream2, h->sfork_ev, 0));
+  }
+  if (d.nS > 0) {
+    cudaStream_t s2 = fork ? h->stream2 : s;
+    k_solve_p3<<<d.nS, 128, 0, s2>>>(d, h->st); ++nl;
+    k_solve_sep<<<d.nS, 128, 0, s2>>>(d, 0, y, h->st); ++nl;
+    k_solve_sep<<<d.nS, 128, 0, s2>>>(d, 1, y, h->st); ++nl;
+  }
+  if (h->nitems > 0 && nR > 0) {
     mark(h, "trsv_p2_stage_Linv");
     k_gemv_stage<<<h->nsingle + ((h->nitems - h->nsingle) * 32 + TB - 1) / TB, TB, 0, s>>>(
         d, h->items, h->nitems, h->nsingle, h->stage_list, 0, d.u, d.v, h->st);
-    ++nl;
-  }
-  if (d.nS > 0) {
-    mark(h, "trsv_p3_sep_rhs");
-    k_solve_p3<<<d.nS, 128, 0, s>>>(d, h->st); ++nl;
-    mark(h, "trsv_p4_sep_LTinv");
-    k_solve_sep<<<d.nS, 128, 0, s>>>(d, 0, y, h->st); ++nl;
-    mark(h, "trsv_p5_sep_LTinvT");
-    k_solve_sep<<<d.nS, 128, 0, s>>>(d, 1, y, h->st); ++nl;
-  }
-  const int nR = d.S0 - d.nL;
-  if (nR > 0) {
-    if (d.nS > 0) {
-      mark(h, "trsv_p6a_stage_F");
-      k_solve_p6a<<<(nR * 32 + TB - 1) / TB, TB, 0, s>>>(d, h->row_stage_R, y, h->st); ++nl;
-    } else {
-      CK(cudaMemcpyAsync(d.t + d.nL, d.v + d.nL, sizeof(double) * nR, cudaMemcpyDeviceToDevice, s));
-    }
     mark(h, "trsv_p6b_stage_LinvT");
     k_gemv_stage<<<h->nsingle + ((h->nitems - h->nsingle) * 32 + TB - 1) / TB, TB, 0, s>>>(
-        d, h->items, h->nitems, h->nsingle, h->stage_list, 1, d.t, y, h->st);
-    ++nl;
+        d, h->items, h->nitems, h->nsingle, h->stage_list, 1, d.v, d.nS > 0 ? d.t : y, h->st);
+    nl += 2;
+  }
+  if (fork) {
+    CK(cudaEventRecord(h->sjoin_ev, h->stream2));
+    CK(cudaStreamWaitEvent(s, h->sjoin_ev, 0));
+  }
+  if (nR > 0 && d.nS > 0) {
+    mark(h, "trsv_p6a_stage_H");
+    k_solve_p6a<<<(nR * 32 + TB - 1) / TB, TB, 0, s>>>(d, h->row_stage_R, y, h->st); ++nl;
   }
   if (d.nL > 0) { mark(h, "trsv_p7_leaf_bwd"); k_solve_p7<<<(d.nL + TB - 1) / TB, TB, 0, s>>>(d, ra, y, h->st); ++nl; }
   CK(cudaGetLastError());
   return STROM_OK;
 }
-
 
 strom_status launch_eig(strom_admm *h, int mode, const double *yv, int &nl) {
   // Size classes are independent: the largest class runs on the main stream, the
@@ -737,6 +744,7 @@ strom_status transpose_into(strom_admm *h, int rows, int cols, const double *in,
 
 strom_status device_factor_dense(strom_admm *h, std::vector<const double *> &Linv, std::vector<const double *> &LinvT,
                                  std::vector<const double *> &Fp, std::vector<const double *> &Ftp,
+                                 std::vector<const double *> &Hp, std::vector<const double *> &Htp,
                                  std::vector<int32_t> &un, std::vector<int32_t> &uw, double *&LTinv, double *&LTinvT) {
   const Factor &F = h->F;
   SolverHandles H;
@@ -774,9 +782,19 @@ strom_status device_factor_dense(strom_admm *h, std::vector<const double *> &Lin
     }
     Fcm[u] = Fd;
     Ftp[u] = Fd;                                     // column-major F == row-major F^T
-    double *Fr = nullptr;
-    if ((st = transpose_into(h, w, nk, Fd, Fr))) return st;   // (w x nk) row-major -> F row-major
-    Fp[u] = Fr;
+    Fp[u] = nullptr;                                 // row-major F is not needed by the kernels
+    // H = L^{-T} F (column-major n_k x w == row-major H^T), and row-major H
+    double *Hd = nullptr;
+    if ((st = h->alloc(Hd, std::max<size_t>((size_t)nk * w, 1)))) return st;
+    if (nk > 0 && w > 0) {
+      const double one = 1.0;
+      CBLAS(cublasDtrmm(H.blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, nk, w,
+                        &one, A, nk, Fd, nk, Hd, nk));
+    }
+    Htp[u] = Hd;
+    double *Hr = nullptr;
+    if ((st = transpose_into(h, w, nk, Hd, Hr))) return st;
+    Hp[u] = Hr;
   }
   // separator Schur complement T = K'_SS - sum_k F_k^T F_k, then L_T^{-1}
   const int nS = F.T0.rows;
@@ -907,15 +925,16 @@ strom_status strom_admm_setup(strom_admm **out, const strom_sdp *sdp_h, const st
   d.R_off = p_Roff; d.S_off = p_Soff; d.stage_uid = p_suid; d.stage_wl = p_swl; d.stage_wr = p_swr;
   // ---- dense factors: computed on the device (setup only) -------------------------
   const int nu = (int)F.uK.size();
-  std::vector<const double *> hLinv(nu), hLinvT(nu), hF(nu), hFt(nu);
+  std::vector<const double *> hLinv(nu), hLinvT(nu), hF(nu), hFt(nu), hH(nu), hHt(nu);
   std::vector<int32_t> un(nu), uw(nu);
   double *dLTinv = nullptr, *dLTinvT = nullptr;
-  if ((st = device_factor_dense(h.get(), hLinv, hLinvT, hF, hFt, un, uw, dLTinv, dLTinvT))) return st;
-  const double **pp1, **pp2, **pp3, **pp4;
+  if ((st = device_factor_dense(h.get(), hLinv, hLinvT, hF, hFt, hH, hHt, un, uw, dLTinv, dLTinvT))) return st;
+  const double **pp1, **pp2, **pp3, **pp4, **pp5, **pp6;
   if ((st = h->upload(pp1, hLinv)) || (st = h->upload(pp2, hLinvT)) || (st = h->upload(pp3, hF)) ||
-      (st = h->upload(pp4, hFt)) || (st = h->upload(p_un, un)) || (st = h->upload(p_uw, uw)))
+      (st = h->upload(pp4, hFt)) || (st = h->upload(pp5, hH)) || (st = h->upload(pp6, hHt)) ||
+      (st = h->upload(p_un, un)) || (st = h->upload(p_uw, uw)))
     return st;
-  d.Linv = pp1; d.LinvT = pp2; d.F = pp3; d.Ft = pp4; d.uid_n = p_un; d.uid_w = p_uw;
+  d.Linv = pp1; d.LinvT = pp2; d.F = pp3; d.Ft = pp4; d.H = pp5; d.Ht = pp6; d.uid_n = p_un; d.uid_w = p_uw;
   d.LTinv = dLTinv; d.LTinvT = dLTinvT;
   if ((st = h->alloc(d.u, m)) || (st = h->alloc(d.v, m)) || (st = h->alloc(d.t, m)) || (st = h->alloc(d.z, m)))
     return st;
@@ -964,11 +983,11 @@ strom_status strom_admm_setup(strom_admm **out, const strom_sdp *sdp_h, const st
       const double w = (double)h->eig_class_blocks[c].size() * nps[c] * nps[c] * nps[c];
       if (w > best) { best = w; h->eig_main_class = (int)c; }
     }
-    if (nps.size() > 1) {
-      CK(cudaStreamCreateWithFlags(&h->stream2, cudaStreamNonBlocking));
-      CK(cudaEventCreateWithFlags(&h->fork_ev, cudaEventDisableTiming));
-      CK(cudaEventCreateWithFlags(&h->join_ev, cudaEventDisableTiming));
-    }
+    CK(cudaStreamCreateWithFlags(&h->stream2, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&h->fork_ev, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&h->join_ev, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&h->sfork_ev, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&h->sjoin_ev, cudaEventDisableTiming));
     for (size_t c = 0; c < nps.size(); ++c) {
       int32_t *pd;
       if ((st = h->upload(pd, h->eig_class_blocks[c]))) return st;

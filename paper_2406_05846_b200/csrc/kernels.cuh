@@ -44,6 +44,7 @@ struct SolveDev {
   // F (n_k x w), Ft (w x n_k)
   const double *const *Linv; const double *const *LinvT;
   const double *const *F; const double *const *Ft;
+  const double *const *H; const double *const *Ht;   // H_k = L_k^{-T} F_k (n_k x w), H^T
   const int32_t *uid_n, *uid_w;
   const double *LTinv, *LTinvT;   // nS x nS
   // work vectors (internal order, length m)
