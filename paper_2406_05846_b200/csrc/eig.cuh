@@ -49,6 +49,37 @@ __device__ __forceinline__ double rcp_approx(double x) {
   return r;
 }
 
+// Jacobi rotation for a column pair with ||u_p||^2 = al, ||u_q||^2 = be, u_p.u_q = ga:
+// t = tan(theta) = sign(d) g2 / (|d| + sqrt(d^2 + g2^2)), d = be - al, g2 = 2 ga; t needs
+// ~1e-10 relative accuracy only, (cs, sn) are orthogonal to fp64 precision.
+__device__ __forceinline__ void jacobi_cs(double al, double be, double ga, double &cs, double &sn) {
+  const double d = be - al, g2 = 2.0 * ga;
+  const double h2 = fma(d, d, g2 * g2);
+  double rh = rsqrt_approx(h2);
+  rh = rh * fma(-0.5 * h2, rh * rh, 1.5);
+  const double den = fabs(d) + h2 * rh;
+  double rc = rcp_approx(den);
+  rc = rc * fma(-den, rc, 2.0);
+  const double t = (d >= 0.0 ? g2 : -g2) * rc;
+  const double t2 = t * t;
+  if (t2 < 1e-8) {
+    cs = fma(t2, fma(t2, 0.375, -0.5), 1.0);
+  } else {
+    const double y = 1.0 + t2;
+    cs = rsqrt_approx(y);
+    cs = cs * fma(-0.5 * y, cs * cs, 1.5);
+    cs = cs * fma(-0.5 * y, cs * cs, 1.5);
+  }
+  sn = cs * t;
+}
+
+template <int G>
+__device__ __forceinline__ double group_sum(double v) {
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
 __device__ __forceinline__ int svec_pos(int i, int j) {  // i, j any order
   return (i <= j) ? (j * (j + 1) / 2 + i) : (i * (i + 1) / 2 + j);
 }
@@ -333,4 +364,258 @@ inline int eig_threads(int n) {
   while (t < 512 && (int64_t)n * n > 16LL * t) t += 32;   // warm-start product capacity
   if (n > 16) t = std::max(t, 256);
   return std::min(t, 512);
+}
+
+// ============================================================================
+// K-EIG, cluster variant for orders 113..236 (car back-in / landing 190, flying robot
+// 231). A 2-CTA cluster owns one block: CTA r holds rows
+// [r*h, r*h + h) of U = X_b + sI (h = ceil(n/2)) for all n columns in its shared memory.
+// Per round each CTA computes the partial dots u_p.u_q over its rows for every pair,
+// publishes them in its shared memory, one cluster barrier, then both CTAs read both
+// partials through DSMEM, sum them in a fixed order (identical in both CTAs), compute the
+// same rotation and apply it to their own rows. Column norms are kept identical in both
+// CTAs. Cold start (V = I) in this version; eigenvectors = normalised columns of U.
+// ============================================================================
+constexpr int kClusterEig = 2;
+
+__host__ __device__ inline int eig_cluster_rows(int n) { return (n + kClusterEig - 1) / kClusterEig; }
+inline bool eig_use_cluster(int n) { return n > 112 && n <= 236; }
+inline size_t eig_cluster_smem_bytes(int n) {
+  const int NP = n + (n & 1), H = NP / 2, h = eig_cluster_rows(n);
+  return sizeof(double) * ((size_t)h * n + n /*norms*/ + n /*lambda*/ + 2 * (size_t)H /*partials*/ + 16);
+}
+
+__global__ void __cluster_dims__(kClusterEig, 1, 1) __launch_bounds__(512, 1) k_eig_cluster(EigArgs a) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  if (a.st->done) return;                     // uniform across the cluster
+  extern __shared__ double sm[];
+  __shared__ double red[4 * 32];
+  __shared__ int sets[128];
+  __shared__ int set_info;
+  constexpr int G = 16, EPL = 8, PPW = 32 / G;   // h <= 118 rows per CTA -> 8 rows per lane
+  const int crank = (int)cl.block_rank();
+  const int bidx = a.blocks[blockIdx.x / kClusterEig];
+  const int n = a.bn[bidx];
+  const int NP = n + (n & 1), H = NP / 2;
+  const int h = eig_cluster_rows(n);
+  const int r0 = crank * h, nloc = min(h, n - r0);   // local rows [r0, r0 + nloc)
+  const int64_t off = a.boff[bidx];
+  const int L = n * (n + 1) / 2;
+  double *U = sm;                                   // column j, local row i: U[j*h + i]
+  double *nrm = sm + (size_t)h * n;                 // n
+  double *lamv = nrm + n;                           // n
+  double *part = lamv + n;                          // 2 x H (parity)
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5, nwarps = nt >> 5;
+  const int grp = lane / G, sub = lane % G;
+  const double sigma = a.st->sigma;
+  const double isq2 = 0.70710678118654752440;
+  const bool proj = (a.mode == 0);
+  // ---- 1. gather X_b (each CTA half of the svec entries), Frobenius norm -------------
+  double fro = 0.0;
+  for (int e = crank * nt + tid; e < L; e += kClusterEig * nt) {
+    const int64_t J = off + e;
+    double aty = 0.0;
+    for (int64_t t = a.Atp[J]; t < a.Atp[J + 1]; ++t) aty += a.Atv[t] * a.y[a.Atr[t]];
+    const double xb = proj ? a.X[J] + sigma * (aty - a.C[J]) : a.C[J] - aty;
+    a.Xb_out[J] = xb;
+    fro += xb * xb;
+  }
+  {
+    double v1[1] = {fro};
+    block_sum<1>(v1, red);
+    if (tid == 0) part[0] = v1[0];
+  }
+  cl.sync();                                        // Xb_out and both partial norms visible
+  double s;
+  {
+    double tot = 0.0;
+    for (int c = 0; c < kClusterEig; ++c) tot += cl.map_shared_rank(part, c)[0];
+    s = 2.0 * sqrt(tot) + 1e-300;
+  }
+  cl.sync();                                        // partial slot reused below
+  const double *Xb = a.Xb_out + off;
+  // ---- 2. local rows of U = (X_b + sI) V, V = V_prev (warm) or I ------------------------
+  const bool warm = proj && a.warm_enable && a.st->eig_warm_valid &&
+                    (a.cold_every <= 0 || (a.st->iter % a.cold_every) != 0);
+  if (warm) {
+    // U[i, j] = sum_k A[i, k] V[k, j] + s V[i, j]; A from the L2-resident svec X_b, V_prev
+    // column-major in global memory (column j is a warp-uniform broadcast stream)
+    const double *Vp = a.Vstore + a.voff[bidx];
+    for (int e = tid; e < nloc * n; e += nt) {
+      const int j = e / nloc, il = e - j * nloc, i = r0 + il;
+      const double *vj = Vp + (int64_t)j * n;
+      double t0 = 0.0, t1 = 0.0;
+      int k = 0;
+      for (; k + 1 < n; k += 2) {
+        const double a0 = Xb[svec_pos(i, k)], a1 = Xb[svec_pos(i, k + 1)];
+        t0 += (i == k ? a0 : a0 * isq2) * vj[k];
+        t1 += (i == k + 1 ? a1 : a1 * isq2) * vj[k + 1];
+      }
+      if (k < n) { const double a0 = Xb[svec_pos(i, k)]; t0 += (i == k ? a0 : a0 * isq2) * vj[k]; }
+      U[j * h + il] = (t0 + t1) + s * vj[i];
+    }
+  } else {
+    for (int e = tid; e < nloc * n; e += nt) {
+      const int j = e / nloc, il = e - j * nloc, i = r0 + il;
+      const double v = Xb[svec_pos(i, j)];
+      U[j * h + il] = (i == j) ? v + s : v * isq2;
+    }
+  }
+  __syncthreads();
+  cl.sync();          // every CTA has read V_prev before anyone overwrites it (step 4)
+  // ---- 3. sweeps ------------------------------------------------------------------------
+  const double tol = fmax(a.tol, 4.0 * n * 2.220446049250313e-16);
+  const double tol2 = tol * tol, quad2 = 1e-18;
+  bool converged = false;
+  int sweep = 0;
+  for (; sweep < a.max_sweeps; ++sweep) {
+    // exact column norms: partial over local rows, exchanged through DSMEM
+    for (int j = warp; j < n; j += nwarps) {
+      const double *uj = U + j * h;
+      double t = 0.0;
+      for (int i = lane; i < nloc; i += 32) t += uj[i] * uj[i];
+      t = warp_sum(t);
+      if (lane == 0) lamv[j] = t;
+    }
+    cl.sync();
+    for (int j = tid; j < n; j += nt) {
+      double t = 0.0;
+      for (int c = 0; c < kClusterEig; ++c) t += cl.map_shared_rank(lamv, c)[j];
+      nrm[j] = t;
+    }
+    cl.sync();                                      // lamv free again; nrm complete
+    int rotated = 0, big = 0;
+    for (int r = 0; r < NP - 1; ++r) {
+      double *pr = part + (r & 1) * H;
+      // phase A: partial dots over the local rows
+      for (int P0 = warp * PPW; P0 < H; P0 += nwarps * PPW) {
+        const int P = P0 + grp;
+        int p = 0, q = 0;
+        bool valid = P < H;
+        if (valid) {
+          p = rr_pos(P, r, NP - 1); q = rr_pos(NP - 1 - P, r, NP - 1);
+          if (p > q) { const int t2 = p; p = q; q = t2; }
+          valid = q < n;
+        }
+        double g0 = 0.0, g1 = 0.0;
+        if (valid) {
+          const double *up = U + p * h, *uq = U + q * h;
+#pragma unroll
+          for (int c = 0; c < EPL; ++c) {
+            const int i = sub + G * c;
+            if (i < nloc) { if (c & 1) g1 += up[i] * uq[i]; else g0 += up[i] * uq[i]; }
+          }
+        }
+        const double ga = group_sum<G>(g0 + g1);
+        if (valid && sub == 0) pr[P] = ga;
+      }
+      cl.sync();
+      // phase B: identical rotations in both CTAs, applied to the local rows
+      for (int P0 = warp * PPW; P0 < H; P0 += nwarps * PPW) {
+        const int P = P0 + grp;
+        if (P >= H) continue;
+        int p = rr_pos(P, r, NP - 1), q = rr_pos(NP - 1 - P, r, NP - 1);
+        if (p > q) { const int t2 = p; p = q; q = t2; }
+        if (q >= n) continue;
+        double ga = 0.0;
+        for (int c = 0; c < kClusterEig; ++c) ga += cl.map_shared_rank(pr, c)[P];
+        const double al = nrm[p], be = nrm[q];
+        const double ab = al * be, g2a = ga * ga;
+        if (ga != 0.0 && g2a > tol2 * ab) {
+          rotated = 1;
+          if (g2a > quad2 * ab) big = 1;
+          double cs, sn;
+          jacobi_cs(al, be, ga, cs, sn);
+          double *up = U + p * h, *uq = U + q * h;
+#pragma unroll
+          for (int c = 0; c < EPL; ++c) {
+            const int i = sub + G * c;
+            if (i < nloc) {
+              const double x = up[i], y = uq[i];
+              up[i] = cs * x - sn * y; uq[i] = sn * x + cs * y;
+            }
+          }
+          if (sub == 0) {
+            const double c2 = cs * cs, s2 = sn * sn, csn = 2.0 * cs * sn * ga;
+            nrm[p] = c2 * al - csn + s2 * be;
+            nrm[q] = s2 * al + csn + c2 * be;
+          }
+        }
+      }
+      __syncthreads();
+    }
+    const int any_big = __syncthreads_or(big);
+    const int any_rot = __syncthreads_or(rotated);
+    if (!any_rot || !any_big) { converged = true; break; }
+  }
+  if (tid == 0 && crank == 0) {
+    if (!converged) atomicCAS(&a.st->eig_fail, 0, bidx + 1);
+    atomicAdd(&a.st->eig_sweeps, (unsigned long long)(sweep + 1));
+  }
+  // ---- 4. eigenpairs: exact norms (DSMEM), lambda = ||u|| - s, V = normalised U --------
+  for (int j = warp; j < n; j += nwarps) {
+    const double *uj = U + j * h;
+    double t = 0.0;
+    for (int i = lane; i < nloc; i += 32) t += uj[i] * uj[i];
+    t = warp_sum(t);
+    if (lane == 0) lamv[j] = t;
+  }
+  cl.sync();
+  for (int j = tid; j < n; j += nt) {
+    double t = 0.0;
+    for (int c = 0; c < kClusterEig; ++c) t += cl.map_shared_rank(lamv, c)[j];
+    nrm[j] = sqrt(t);                               // ||u_j||
+  }
+  cl.sync();
+  for (int j = tid; j < n; j += nt) lamv[j] = nrm[j] - s;
+  __syncthreads();
+  const double *lam = lamv;
+  if (!proj) {
+    if (tid == 0 && crank == 0) {
+      double lm = lam[0];
+      for (int k = 1; k < n; ++k) lm = fmin(lm, lam[k]);
+      a.lam_min[bidx] = lm;
+    }
+    return;
+  }
+  // normalised local rows -> global V (column-major n x n) for the reconstruction
+  double *Vg = a.Vstore + a.voff[bidx];
+  for (int e = tid; e < nloc * n; e += nt) {
+    const int j = e / nloc, il = e - j * nloc;
+    Vg[j * n + r0 + il] = U[j * h + il] / nrm[j];
+  }
+  if (tid == 0) {
+    int npos = 0, nneg = 0;
+    for (int k = 0; k < n; ++k) { if (lam[k] > 0.0) ++npos; else if (lam[k] < 0.0) ++nneg; }
+    const int use_pos = npos <= nneg;
+    int cnt = 0;
+    for (int k = 0; k < n; ++k)
+      if (use_pos ? (lam[k] > 0.0) : (lam[k] < 0.0)) sets[cnt++] = k;
+    set_info = cnt * 2 + use_pos;
+  }
+  __threadfence();
+  cl.sync();                                        // V rows of both CTAs visible in global
+  const int cnt = set_info >> 1, use_pos = set_info & 1;
+  const double is = 1.0 / sigma;
+  for (int e = crank * nt + tid; e < L; e += kClusterEig * nt) {
+    int j = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+    while (j * (j + 1) / 2 > e) --j;
+    while ((j + 1) * (j + 2) / 2 <= e) ++j;
+    const int i = e - j * (j + 1) / 2;
+    double acc = 0.0;
+    for (int c = 0; c < cnt; ++c) {
+      const int k = sets[c];
+      acc += lam[k] * Vg[k * n + i] * Vg[k * n + j];
+    }
+    double sv;
+    if (use_pos) {
+      const double xb = Xb[e];
+      sv = (acc - (i == j ? xb : xb * isq2)) * is;
+    } else {
+      sv = -acc * is;
+    }
+    a.S_out[off + e] = (i == j) ? sv : sv * 1.41421356237309504880;
+  }
 }

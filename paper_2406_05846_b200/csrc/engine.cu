@@ -11,6 +11,7 @@
 //   finalize                      -> eta, sigma policy, done flag
 // Step 1 needs A(X^k) and A(S^k) only, which the previous iteration produced, so
 // Step 1 costs no SpMV.
+#include <cooperative_groups.h>
 #include <cublas_v2.h>
 #include <cuda_runtime.h>
 #include <cusolverDn.h>
@@ -390,6 +391,7 @@ struct strom_admm {
   std::vector<std::vector<int32_t>> eig_class_blocks;
   std::vector<int32_t *> eig_class_dev;
   std::vector<int> eig_class_np;
+  std::vector<int> eig_class_n;              // max block order in the class
   int eig_main_class = 0;                    // class with the largest n^3 work
   cudaStream_t stream2 = nullptr;            // fork for concurrent eig size classes
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr, sfork_ev = nullptr, sjoin_ev = nullptr;
@@ -538,7 +540,9 @@ strom_status launch_eig(strom_admm *h, int mode, const double *yv, int &nl) {
     if (s == h->stream) mark(h, eig_names[c < 8 ? c : 7]);
     a.Ug = h->Ug; a.Ag = h->Ag; a.uoff = h->uoff;
     const int G = eig_G(np);
-    if (eig_global(np)) k_eig<32, 8, true><<<a.nblk, threads, smem, s>>>(a);
+    if (eig_use_cluster(h->eig_class_n[c])) {
+      k_eig_cluster<<<a.nblk * kClusterEig, 512, eig_cluster_smem_bytes(h->eig_class_n[c]), s>>>(a);
+    } else if (eig_global(np)) k_eig<32, 8, true><<<a.nblk, threads, smem, s>>>(a);
     else if (G == 4) k_eig<4, 4, false><<<a.nblk, threads, smem, s>>>(a);
     else if (G == 8) k_eig<8, 8, false><<<a.nblk, threads, smem, s>>>(a);
     else if (G == 32) k_eig<32, 2, false><<<a.nblk, threads, smem, s>>>(a);
@@ -978,6 +982,14 @@ strom_status strom_admm_setup(strom_admm **out, const strom_sdp *sdp_h, const st
       else h->eig_class_blocks[it - nps.begin()].push_back(k);
     }
     h->eig_class_np = nps;
+    for (size_t c = 0; c < nps.size(); ++c) {
+      int mx = 0;
+      for (int k : h->eig_class_blocks[c]) mx = std::max(mx, s.bn[k]);
+      h->eig_class_n.push_back(mx);
+      if (eig_use_cluster(mx))
+        CK(cudaFuncSetAttribute(k_eig_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)eig_cluster_smem_bytes(mx)));
+    }
     double best = -1.0;
     for (size_t c = 0; c < nps.size(); ++c) {
       const double w = (double)h->eig_class_blocks[c].size() * nps[c] * nps[c] * nps[c];
