@@ -1,0 +1,33 @@
+"""Product-side certificate (host post-processing) against the
+oracle's independent extraction on a solved pendulum instance."""
+import numpy as np
+
+from oracle import Oracle, extract_pendulum, lower_bound
+from paper_2406_05846_b200 import certify
+from strom_inputs import compile_relaxation, lift_rank1, models
+
+
+def test_certificate_matches_oracle_extraction():
+    sdp = compile_relaxation(models.pendulum(4, 0.3, 1.0))
+    o = Oracle(sdp)
+    it, ok = o.solve_to_tol(1e-6, 20000)
+    assert ok
+    p1, z1, f1 = certify.pendulum_upper_bound(sdp, o.X)
+    z2, p2, f2 = extract_pendulum(sdp, o.X)
+    assert f1 and f2 and abs(p1 - p2) <= 1e-8 * (1 + abs(p2))
+    LB, _ = lower_bound(sdp, o.y, o.apply_At(o.y))
+    xi = certify.suboptimality_gap(p1, LB)
+    assert 0.0 <= xi < 1e-2
+    # the rounded point is feasible: A(X(z_hat)) = b
+    import scipy.sparse as sp
+    A = sp.csr_matrix((sdp.A_data, sdp.A_indices, sdp.A_indptr), shape=(sdp.m, sdp.n))
+    assert np.max(np.abs(A @ lift_rank1(sdp, z1) - sdp.b)) < 1e-10
+
+
+def test_extract_zbar_recovers_rank_one_point():
+    """For X = X(z) exactly rank one, extraction returns z (Theorem 1(iii))."""
+    sdp = compile_relaxation(models.pendulum(3, 0.5, -1.0))
+    rng = np.random.default_rng(0)
+    z = models.pendulum_rollout(3, rng.uniform(-0.3, 0.3, 3), 0.5, -1.0)
+    zbar = certify.extract_zbar(sdp, lift_rank1(sdp, z))
+    assert np.allclose(zbar, z, atol=1e-10)
