@@ -238,3 +238,34 @@ def test_large_block_iterations_parity(name):
     _compare(g, o, 1e-9, f"{name}@5")
     g.iterate(15); o.iterate(15)
     _compare(g, o, 1e-9, f"{name}@20")
+
+
+@pytest.mark.parametrize("shape,N", [("carback", 30), ("flying", 60), ("cartpole", 30)])
+def test_full_size_properties(shape, N):
+    """BASELINE configs[2..4] at full size in the bench's launch configuration, checked by
+    properties that hold at any size (the oracle is too slow here):
+      F3: A(X^{k+1}) - b = (1 - tau)(A(X^k) - b) - tau sigma eps y^{k+1}
+      S^{k+1} in Omega_+ (sampled blocks) and eta recomputed on the host from (X, y, S)."""
+    import scipy.sparse as sp
+    sdp = compile_relaxation(models.synthetic_shape(shape, N, seed=0))
+    g = make(sdp, check_every=10)
+    A = sp.csr_matrix((sdp.A_data, sdp.A_indices, sdp.A_indptr), shape=(sdp.m, sdp.n))
+    g.iterate(4)
+    X4, _, _, _ = g.get(y=False, S=False)
+    g.iterate(1)
+    X5, y5, S5, res = g.get()
+    tau, sigma, eps = 1.618, 1.0, g.eps()
+    lhs = A @ X5 - sdp.b
+    rhs = (1 - tau) * (A @ X4 - sdp.b) - tau * sigma * eps * y5
+    assert np.linalg.norm(lhs - rhs) <= 1e-9 * (1 + np.linalg.norm(A @ X4 - sdp.b))
+    bo = sdp.block_offset
+    rng = np.random.default_rng(0)
+    for beta in rng.choice(sdp.nblocks, size=8, replace=False):
+        nb = int(sdp.block_n[beta])
+        Sb = svec_to_mat(S5[bo[beta]:bo[beta + 1]], nb)
+        assert np.linalg.eigvalsh(Sb)[0] >= -1e-9 * (1 + np.abs(Sb).max())
+    Aty = A.T @ y5
+    eta_d = np.linalg.norm(Aty + S5 - sdp.C) / (1 + np.linalg.norm(sdp.C))
+    eta_p = np.linalg.norm(A @ X5 - sdp.b) / (1 + np.linalg.norm(sdp.b))
+    assert abs(eta_d - res["eta_d"]) <= 1e-6 * eta_d + 1e-14
+    assert abs(eta_p - res["eta_p"]) <= 1e-6 * eta_p + 1e-14
