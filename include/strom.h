@@ -111,10 +111,17 @@ typedef struct {
 void strom_admm_default_config(strom_admm_config *cfg);
 
 /* Builds eps I + AA*, orders rows (leaf pairs, stage interiors, separators),
- * factors once on the host (eq:strom:gpu:cholesky) and uploads everything to
- * `device`. `cuda_stream` is a cudaStream_t (NULL = the handle creates its own);
- * e.g. torch.cuda.current_stream().cuda_stream. Multi-GPU horizon partitioning
- * (nccl_unique_id != NULL, nranks > 1) returns ENOTIMPL in this version.
+ * factors once (eq:strom:gpu:cholesky; dense blocks on the device at setup) and uploads
+ * everything to `device`. `cuda_stream` is a cudaStream_t (NULL = the handle creates its
+ * own), e.g. a torch.cuda.Stream().cuda_stream.
+ * Multi-GPU (nranks > 1, one process per GPU, every rank passes the same SDP and the same
+ * 128-byte NCCL unique id from strom_nccl_get_unique_id on rank 0): the PSD projection --
+ * the step that "dominates the runtime" and that the paper distributes over GPUs
+ * -- is split by contiguous stage ranges balanced by sum n_beta^3; after
+ * K-EIG every rank's S and X_b segments are exchanged with NCCL broadcasts captured in the
+ * iteration graph; the rest of the iteration is replicated (identical on every rank), so
+ * strom_admm_get returns the full iterate on every rank. EINVAL if nranks > 1 without an
+ * id or nranks > number of stages; ENCCL on communicator errors.
  * Starts cold: X = S = 0 (reading Q13). */
 strom_status strom_admm_setup(strom_admm **out, const strom_sdp *sdp, const strom_admm_config *cfg,
                               int device, void *cuda_stream, const void *nccl_unique_id,
@@ -176,6 +183,7 @@ strom_status strom_admm_factor_info(const strom_admm *h, int64_t *device_bytes,
  * number of launches per iteration, or a negative strom_status. */
 int32_t strom_admm_kernel_times(strom_admm *h, double *ms, const char **names, int32_t cap);
 
+/* rank 0: fills the 128-byte NCCL unique id to broadcast (e.g. via torch.distributed). */
 strom_status strom_nccl_get_unique_id(void *id128);
 const char *strom_last_error(void);
 const char *strom_version(void);
@@ -196,6 +204,11 @@ strom_status strom_debug_host_solve(const strom_sdp *sdp, const strom_admm_confi
                                     const double *r, double *y);
 /* eps actually used by a handle. */
 double strom_debug_eps(const strom_admm *h);
+/* In-process "virtual ranks": nranks handles of the same SDP on one device play the
+ * ranks of the multi-GPU mode; the exchange is a device-to-device copy instead of NCCL.
+ * link: partition the projection; iterate: `iters` lock-step iterations of all handles. */
+strom_status strom_debug_link_virtual(strom_admm **handles, int32_t nranks, const strom_sdp *sdp);
+strom_status strom_debug_iterate_virtual(strom_admm **handles, int32_t nranks, int64_t iters);
 
 #ifdef __cplusplus
 }

@@ -30,7 +30,7 @@ EXPORTS = [
     "strom_admm_get_device", "strom_admm_lower_bound", "strom_admm_launches_per_iter",
     "strom_admm_factor_info", "strom_admm_kernel_times", "strom_nccl_get_unique_id", "strom_last_error", "strom_version",
     "strom_debug_project_psd", "strom_debug_spmv", "strom_debug_solve", "strom_debug_host_solve",
-    "strom_debug_eps",
+    "strom_debug_eps", "strom_debug_link_virtual", "strom_debug_iterate_virtual",
 ]
 
 
@@ -101,6 +101,8 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "strom_debug_solve": (I32, [VP, P(D), P(D)]),
         "strom_debug_host_solve": (I32, [VP, P(strom_admm_config), P(D), P(D)]),
         "strom_debug_eps": (D, [VP]),
+        "strom_debug_link_virtual": (I32, [P(VP), I32, VP]),
+        "strom_debug_iterate_virtual": (I32, [P(VP), I32, I64]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -213,13 +215,19 @@ class StromAdmm:
     """strom_admm_setup and friends on one device / stream."""
 
     def __init__(self, sdp: StromSdp, cfg: Optional[strom_admm_config] = None, device: int = 0,
-                 stream=None):
+                 stream=None, rank: int = 0, nranks: int = 1, nccl_id: Optional[bytes] = None):
+        """nranks > 1: one process per GPU, the same SDP and the same `nccl_id`
+        (strom_nccl_get_unique_id() on rank 0, broadcast by the caller) on every rank;
+        the PSD projection is distributed by stage ranges."""
         lib = load()
         self.sdp = sdp
         self.cfg = cfg or strom_admm_default_config()
         h = C.c_void_p()
+        idbuf = None
+        if nccl_id is not None:
+            idbuf = C.create_string_buffer(bytes(nccl_id), 128)
         _check(lib.strom_admm_setup(C.byref(h), sdp.handle, C.byref(self.cfg), device,
-                                    _torch_stream_ptr(stream), None, 0, 1), "strom_admm_setup")
+                                    _torch_stream_ptr(stream), idbuf, rank, nranks), "strom_admm_setup")
         self.handle = h
         self.n, self.m = sdp.n, sdp.m
 
@@ -316,6 +324,24 @@ class StromAdmm:
         if getattr(self, "handle", None) and _lib is not None:
             _lib.strom_admm_destroy(self.handle)
             self.handle = None
+
+
+def strom_nccl_get_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(load().strom_nccl_get_unique_id(buf), "strom_nccl_get_unique_id")
+    return buf.raw
+
+
+def strom_debug_link_virtual(admms, sdp: StromSdp):
+    """Test harness: len(admms) handles of the same SDP on one device act as the ranks of
+    the multi-GPU mode (exchange by device copies instead of NCCL)."""
+    arr = (C.c_void_p * len(admms))(*[a.handle.value for a in admms])
+    _check(load().strom_debug_link_virtual(arr, len(admms), sdp.handle), "strom_debug_link_virtual")
+
+
+def strom_debug_iterate_virtual(admms, iters: int):
+    arr = (C.c_void_p * len(admms))(*[a.handle.value for a in admms])
+    _check(load().strom_debug_iterate_virtual(arr, len(admms), int(iters)), "strom_debug_iterate_virtual")
 
 
 def strom_version() -> str:

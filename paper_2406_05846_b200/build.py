@@ -50,7 +50,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
             sys.stderr.write(r.stderr)
         objs.append(o)
     cmd = [nvcc, "-shared", "-o", OUT, *objs, *ARCH, "-Xcompiler", "-fopenmp", "-lgomp",
-           "-lcusolver", "-lcublas"]
+           "-lcusolver", "-lcublas", "-lnccl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

@@ -15,6 +15,7 @@
 #include <cublas_v2.h>
 #include <cuda_runtime.h>
 #include <cusolverDn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cstdlib>
@@ -393,6 +394,16 @@ struct strom_admm {
   std::vector<int> eig_class_np;
   std::vector<int> eig_class_n;              // max block order in the class
   int eig_main_class = 0;                    // class with the largest n^3 work
+  // multi-GPU ("we distribute moment matrices for eig"): rank r projects the
+  // blocks of a contiguous stage range; the S and X_b segments are exchanged after K-EIG.
+  int rank = 0, nranks = 1;
+  int xfer = 0;                              // 0 single, 1 NCCL ranks, 2 in-process virtual ranks
+  ncclComm_t comm = nullptr;
+  cudaEvent_t eig_done_ev = nullptr, copy_done_ev = nullptr;
+  std::vector<int64_t> seg_off, seg_cnt;     // svec segment owned by each rank
+  std::vector<int32_t> stage_cut;            // rank r owns stages [cut[r], cut[r+1])
+  std::vector<int32_t *> eig_class_dev_all;  // every block (lower bound, single rank)
+  std::vector<std::vector<int32_t>> eig_class_all;
   cudaStream_t stream2 = nullptr;            // fork for concurrent eig size classes
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr, sfork_ev = nullptr, sjoin_ev = nullptr;
   cudaGraph_t graphK = nullptr, graph1 = nullptr;
@@ -412,6 +423,9 @@ struct strom_admm {
     if (fork_ev) cudaEventDestroy(fork_ev);
     if (sfork_ev) cudaEventDestroy(sfork_ev);
     if (sjoin_ev) cudaEventDestroy(sjoin_ev);
+    if (eig_done_ev) cudaEventDestroy(eig_done_ev);
+    if (copy_done_ev) cudaEventDestroy(copy_done_ev);
+    if (comm) ncclCommDestroy(comm);
     if (join_ev) cudaEventDestroy(join_ev);
     if (stream2) cudaStreamDestroy(stream2);
     if (execK) cudaGraphExecDestroy(execK);
@@ -525,7 +539,10 @@ strom_status launch_eig(strom_admm *h, int mode, const double *yv, int &nl) {
   for (int c = 0; c < ncls; ++c) {
     const int np = h->eig_class_np[c];
     EigArgs a;
-    a.blocks = h->eig_class_dev[c]; a.nblk = (int)h->eig_class_blocks[c].size();
+    const bool all = (mode == 1);               // the lower bound needs every block
+    a.blocks = all ? h->eig_class_dev_all[c] : h->eig_class_dev[c];
+    a.nblk = (int)(all ? h->eig_class_all[c].size() : h->eig_class_blocks[c].size());
+    if (a.nblk == 0) continue;
     a.bn = h->bn; a.boff = h->boff;
     a.Atp = h->Atp; a.Atr = h->Atr; a.Atv = h->Atv;
     a.X = h->X; a.C = h->C; a.y = yv;
@@ -557,19 +574,43 @@ strom_status launch_eig(strom_admm *h, int mode, const double *yv, int &nl) {
   return STROM_OK;
 }
 
-strom_status launch_iteration(strom_admm *h, int &nl_total) {
+// Steps 1-2 (solve, projection of the locally owned blocks)
+strom_status launch_iteration_A(strom_admm *h, int &nl_total) {
+  int nl = 0;
+  nl_total = 0;
+  RhsArgs ra{h->b, h->AX, h->AS, h->AC};
+  strom_status st;
+  if ((st = launch_solve(h, ra, h->yh, nl)) != STROM_OK) return st;       // Step 1
+  nl_total += nl;
+  if ((st = launch_eig(h, 0, h->yh, nl)) != STROM_OK) return st;         // Step 2 (A* fused)
+  nl_total += nl;
+  return STROM_OK;
+}
+
+// NCCL exchange of every rank's S and X_b segment (in-place broadcasts, one group)
+strom_status nccl_exchange(strom_admm *h) {
+  if (ncclGroupStart() != ncclSuccess) { set_error("ncclGroupStart"); return STROM_ENCCL; }
+  for (int r = 0; r < h->nranks; ++r) {
+    double *sp = h->S + h->seg_off[r], *xp = h->Xb + h->seg_off[r];
+    if (ncclBroadcast(sp, sp, (size_t)h->seg_cnt[r], ncclDouble, r, h->comm, h->stream) != ncclSuccess ||
+        ncclBroadcast(xp, xp, (size_t)h->seg_cnt[r], ncclDouble, r, h->comm, h->stream) != ncclSuccess) {
+      ncclGroupEnd();
+      set_error("ncclBroadcast of the projection segments failed");
+      return STROM_ENCCL;
+    }
+  }
+  if (ncclGroupEnd() != ncclSuccess) { set_error("ncclGroupEnd"); return STROM_ENCCL; }
+  return STROM_OK;
+}
+
+// Steps 3-4 and the residuals
+strom_status launch_iteration_B(strom_admm *h, int &nl_total) {
   cudaStream_t s = h->stream;
   const int TB = 256;
   int nl = 0;
   nl_total = 0;
   RhsArgs ra{h->b, h->AX, h->AS, h->AC};
   strom_status st;
-  // Step 1
-  if ((st = launch_solve(h, ra, h->yh, nl)) != STROM_OK) return st;
-  nl_total += nl;
-  // Step 2 (A*y_half fused into the eig gather)
-  if ((st = launch_eig(h, 0, h->yh, nl)) != STROM_OK) return st;
-  nl_total += nl;
   // Step 3: A S^{k+1}, then solve
   mark(h, "spmv_AS");
   k_spmv<<<(h->m + TB - 1) / TB, TB, 0, s>>>(h->m, h->Arp, h->Aci, h->Av, h->S, h->AS, h->st);
@@ -586,6 +627,61 @@ strom_status launch_iteration(strom_admm *h, int &nl_total) {
   mark(h, nullptr);
   nl_total += 3;
   CK(cudaGetLastError());
+  return STROM_OK;
+}
+
+strom_status launch_iteration(strom_admm *h, int &nl_total) {
+  int na = 0, nb = 0;
+  strom_status st;
+  if ((st = launch_iteration_A(h, na)) != STROM_OK) return st;
+  if (h->xfer == 1 && (st = nccl_exchange(h)) != STROM_OK) return st;
+  if ((st = launch_iteration_B(h, nb)) != STROM_OK) return st;
+  nl_total = na + nb;
+  return STROM_OK;
+}
+
+// Stage ranges balanced by projection work (sum of n^3 over a stage's blocks) and the
+// per-class lists of locally owned blocks. Blocks are stage-sorted, so a rank's blocks
+// (and its svec segment) are contiguous.
+strom_status set_partition(strom_admm *h, const Sdp &s, int rank, int nranks) {
+  const int P = s.nstages;
+  if (nranks < 1 || rank < 0 || rank >= nranks || nranks > P) {
+    set_error("partition: need 1 <= nranks <= number of stages and 0 <= rank < nranks");
+    return STROM_EINVAL;
+  }
+  h->rank = rank; h->nranks = nranks;
+  std::vector<double> cost(P, 1.0);
+  for (int k = 0; k < s.nblocks; ++k) cost[s.bstage[k]] += (double)s.bn[k] * s.bn[k] * s.bn[k];
+  double tot = 0.0;
+  for (double c : cost) tot += c;
+  h->stage_cut.assign(nranks + 1, P);
+  h->stage_cut[0] = 0;
+  double acc = 0.0;
+  int r = 1;
+  for (int k = 0; k < P && r < nranks; ++k) {
+    acc += cost[k];
+    const int left = P - (k + 1);                      // stages still unassigned
+    if (acc >= tot * r / nranks || left == nranks - r) h->stage_cut[r++] = k + 1;
+  }
+  h->seg_off.assign(nranks, 0); h->seg_cnt.assign(nranks, 0);
+  for (int q = 0; q < nranks; ++q) {
+    int b0 = s.nblocks, b1 = 0;
+    for (int k = 0; k < s.nblocks; ++k)
+      if (s.bstage[k] >= h->stage_cut[q] && s.bstage[k] < h->stage_cut[q + 1]) { b0 = std::min(b0, k); b1 = k + 1; }
+    if (b1 > b0) { h->seg_off[q] = s.boff[b0]; h->seg_cnt[q] = s.boff[b1] - s.boff[b0]; }
+  }
+  strom_status st;
+  for (size_t c = 0; c < h->eig_class_all.size(); ++c) {
+    std::vector<int32_t> own;
+    for (int k : h->eig_class_all[c])
+      if (s.bstage[k] >= h->stage_cut[rank] && s.bstage[k] < h->stage_cut[rank + 1]) own.push_back(k);
+    h->eig_class_blocks[c] = own;
+    int32_t *pd = nullptr;
+    if (!own.empty() && (st = h->upload(pd, own))) return st;
+    h->eig_class_dev[c] = pd;
+  }
+  if (!h->eig_done_ev) CK(cudaEventCreateWithFlags(&h->eig_done_ev, cudaEventDisableTiming));
+  if (!h->copy_done_ev) CK(cudaEventCreateWithFlags(&h->copy_done_ev, cudaEventDisableTiming));
   return STROM_OK;
 }
 
@@ -832,11 +928,10 @@ strom_status strom_admm_setup(strom_admm **out, const strom_sdp *sdp_h, const st
                               int nranks) {
   if (!out || !sdp_h || !cfg) { set_error("strom_admm_setup: NULL argument"); return STROM_EINVAL; }
   *out = nullptr;
-  if (nccl_unique_id != nullptr || nranks > 1) {
-    set_error("strom_admm_setup: horizon-partitioned multi-GPU is not built in this version");
-    return STROM_ENOTIMPL;
+  if (nranks > 1 && nccl_unique_id == nullptr) {
+    set_error("strom_admm_setup: nranks > 1 needs an NCCL unique id (strom_nccl_get_unique_id)");
+    return STROM_EINVAL;
   }
-  (void)rank;
   if (!(cfg->sigma > 0.0) || !(cfg->tau > 0.0 && cfg->tau < 2.0) ||
       !(cfg->eps > 0.0 || cfg->eps_rel > 0.0) || cfg->check_every <= 0 || cfg->eig_max_sweeps <= 0) {
     set_error("strom_admm_setup: need sigma > 0, tau in (0,2), eps or eps_rel > 0, check_every > 0");
@@ -1004,6 +1099,8 @@ strom_status strom_admm_setup(strom_admm **out, const strom_sdp *sdp_h, const st
       int32_t *pd;
       if ((st = h->upload(pd, h->eig_class_blocks[c]))) return st;
       h->eig_class_dev.push_back(pd);
+      h->eig_class_dev_all.push_back(pd);
+      h->eig_class_all.push_back(h->eig_class_blocks[c]);
     }
     size_t maxsm = 0;
     for (int np : nps) maxsm = std::max(maxsm, eig_smem_bytes(np));
@@ -1037,6 +1134,17 @@ strom_status strom_admm_setup(strom_admm **out, const strom_sdp *sdp_h, const st
   k_spmv<<<(m + TB - 1) / TB, TB, 0, h->stream>>>(m, h->Arp, h->Aci, h->Av, h->C, h->AC, nullptr);
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(h->stream));
+  // ---- multi-GPU: NCCL communicator and the projection partition ----------------
+  if (nranks > 1) {
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_unique_id, sizeof(id));
+    if (ncclCommInitRank(&h->comm, nranks, id, rank) != ncclSuccess) {
+      set_error("ncclCommInitRank failed");
+      return STROM_ENCCL;
+    }
+    if ((st = set_partition(h.get(), s, rank, nranks))) return st;
+    h->xfer = 1;
+  }
   // ---- graphs ---------------------------------------------------------------
   h->prof_ev.resize(kMaxProfEvents);
   h->prof_names.assign(kMaxProfEvents, nullptr);
@@ -1208,9 +1316,58 @@ strom_status strom_admm_factor_info(const strom_admm *h, int64_t *device_bytes, 
 }
 
 strom_status strom_nccl_get_unique_id(void *id128) {
-  (void)id128;
-  set_error("strom_nccl_get_unique_id: NCCL horizon partitioning not built in this version");
-  return STROM_ENOTIMPL;
+  if (!id128) { set_error("strom_nccl_get_unique_id: NULL"); return STROM_EINVAL; }
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) { set_error("ncclGetUniqueId failed"); return STROM_ENCCL; }
+  std::memcpy(id128, &id, sizeof(id));
+  return STROM_OK;
+}
+
+// ---- in-process virtual ranks (test harness for the multi-GPU exchange) --------------
+strom_status strom_debug_link_virtual(strom_admm **hs, int32_t nranks, const strom_sdp *sdp_h) {
+  if (!hs || nranks < 1 || !sdp_h) { set_error("strom_debug_link_virtual: bad arguments"); return STROM_EINVAL; }
+  const Sdp &s = sdp_of(sdp_h);
+  for (int r = 0; r < nranks; ++r) {
+    strom_status st = set_partition(hs[r], s, r, nranks);
+    if (st) return st;
+    hs[r]->xfer = 2;
+  }
+  return STROM_OK;
+}
+
+strom_status strom_debug_iterate_virtual(strom_admm **hs, int32_t nranks, int64_t iters) {
+  if (!hs || nranks < 1 || iters < 0) { set_error("strom_debug_iterate_virtual: bad arguments"); return STROM_EINVAL; }
+  for (int r = 0; r < nranks; ++r) {
+    const int32_t zero = 0;
+    const double tol = -1.0;
+    CK(cudaMemcpyAsync(&hs[r]->st->done, &zero, sizeof(int32_t), cudaMemcpyHostToDevice, hs[r]->stream));
+    CK(cudaMemcpyAsync(&hs[r]->st->tol, &tol, sizeof(double), cudaMemcpyHostToDevice, hs[r]->stream));
+  }
+  for (int64_t it = 0; it < iters; ++it) {
+    int nl;
+    strom_status st;
+    for (int r = 0; r < nranks; ++r) {      // Steps 1-2 on every rank (own blocks only)
+      strom_admm *h = hs[r];
+      for (int q = 0; q < nranks; ++q)        // peers finished reading our last segment
+        if (q != r) CK(cudaStreamWaitEvent(h->stream, hs[q]->copy_done_ev, 0));
+      if ((st = launch_iteration_A(h, nl))) return st;
+      CK(cudaEventRecord(h->eig_done_ev, h->stream));
+    }
+    for (int r = 0; r < nranks; ++r) {      // exchange the segments, then Steps 3-4
+      strom_admm *h = hs[r];
+      for (int q = 0; q < nranks; ++q) {
+        if (q == r) continue;
+        CK(cudaStreamWaitEvent(h->stream, hs[q]->eig_done_ev, 0));
+        const size_t bytes = sizeof(double) * (size_t)h->seg_cnt[q];
+        CK(cudaMemcpyAsync(h->S + h->seg_off[q], hs[q]->S + h->seg_off[q], bytes, cudaMemcpyDeviceToDevice, h->stream));
+        CK(cudaMemcpyAsync(h->Xb + h->seg_off[q], hs[q]->Xb + h->seg_off[q], bytes, cudaMemcpyDeviceToDevice, h->stream));
+      }
+      CK(cudaEventRecord(h->copy_done_ev, h->stream));
+      if ((st = launch_iteration_B(h, nl))) return st;
+    }
+  }
+  for (int r = 0; r < nranks; ++r) CK(cudaStreamSynchronize(hs[r]->stream));
+  return STROM_OK;
 }
 
 double strom_debug_eps(const strom_admm *h) { return h ? h->F.eps : 0.0; }

@@ -269,3 +269,22 @@ def test_full_size_properties(shape, N):
     eta_p = np.linalg.norm(A @ X5 - sdp.b) / (1 + np.linalg.norm(sdp.b))
     assert abs(eta_d - res["eta_d"]) <= 1e-6 * eta_d + 1e-14
     assert abs(eta_p - res["eta_p"]) <= 1e-6 * eta_p + 1e-14
+
+
+@pytest.mark.parametrize("name,P", [("pend5", 2), ("pend30", 3), ("wide190", 2), ("cartpole", 3)])
+def test_multigpu_partition_virtual_ranks(name, P):
+    """Multi-GPU mode (projection distributed by stage ranges) played by P
+    in-process handles on one device: every rank's iterate equals the single-handle run
+    (the replicated steps are bitwise identical, the exchange moves exact copies)."""
+    sdp = case(name)
+    hs = S.StromSdp(sdp)
+    ref = S.StromAdmm(hs, S.strom_admm_default_config(check_every=5))
+    ranks = [S.StromAdmm(hs, S.strom_admm_default_config(check_every=5)) for _ in range(P)]
+    S.strom_debug_link_virtual(ranks, hs)
+    ref.iterate(12)
+    S.strom_debug_iterate_virtual(ranks, 12)
+    Xr, yr, Sr, rr = ref.get()
+    for g in ranks:
+        X, y, Sg, r = g.get()
+        assert np.array_equal(X, Xr) and np.array_equal(Sg, Sr) and np.array_equal(y, yr)
+        assert r["iter"] == rr["iter"] == 12
