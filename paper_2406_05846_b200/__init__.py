@@ -15,7 +15,8 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libstrom.so")
+# STROM_LIB overrides the in-tree library (A/B timing of two builds)
+LIB_PATH = os.environ.get("STROM_LIB") or os.path.join(_HERE, "libstrom.so")
 
 STATUS = {0: "STROM_OK", 1: "STROM_MAXITER", -1: "STROM_EINVAL", -2: "STROM_ENOMEM",
           -3: "STROM_EFACTOR", -4: "STROM_EEIG", -5: "STROM_EDIVERGED", -6: "STROM_ECUDA",

@@ -84,6 +84,86 @@ __device__ __forceinline__ int svec_pos(int i, int j) {  // i, j any order
   return (i <= j) ? (j * (j + 1) / 2 + i) : (i * (i + 1) / 2 + j);
 }
 
+// X_b = X + sigma (A* y - C) (mode 0) or C - A* y (mode 1) for the svec entries
+// [off + e0, off + L) with stride es, written to Xb_out; returns the partial ||.||^2.
+// Four entries per pass so that their dependent L2 loads (column pointers -> row
+// indices -> y) overlap.
+__device__ __forceinline__ double gather_xb(const EigArgs &a, int64_t off, int L, int e0, int es,
+                                            double sigma, bool proj) {
+  double fro = 0.0;
+  for (int eb = e0; eb < L; eb += 4 * es) {
+    int64_t t0[4], t1[4];
+    double aty[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int e = eb + k * es;
+      t0[k] = t1[k] = 0;
+      if (e < L) { t0[k] = a.Atp[off + e]; t1[k] = a.Atp[off + e + 1]; }
+      aty[k] = 0.0;
+    }
+    for (int r = 0;; ++r) {
+      bool any = false;
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (t0[k] + r < t1[k]) { aty[k] += a.Atv[t0[k] + r] * a.y[a.Atr[t0[k] + r]]; any = true; }
+      if (!any) break;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int e = eb + k * es;
+      if (e < L) {
+        const int64_t J = off + e;
+        const double xb = proj ? a.X[J] + sigma * (aty[k] - a.C[J]) : a.C[J] - aty[k];
+        a.Xb_out[J] = xb;          // mode 1 uses Xb_out as scratch for C - A*y
+        fro += xb * xb;            // svec norm == Frobenius norm
+      }
+    }
+  }
+  return fro;
+}
+
+// Convergence check by the Gram matrix U^T U (4x4 register tiles, upper triangle):
+// true when every pair has (u_i.u_j)^2 <= c2 ||u_i||^2 ||u_j||^2 (norms from nrm).
+// CTA-uniform result (contains a barrier).
+__device__ __forceinline__ bool gram_orthogonal(const double *U, int ld, int n, const double *nrm, double c2,
+                                                int tid, int nt) {
+  const int nT = (n + 3) >> 2, ntile = nT * (nT + 1) / 2;
+  int bad = 0;
+  for (int t = tid; t < ntile; t += nt) {
+    int bi = 0, rem = t;
+    while (rem >= nT - bi) { rem -= nT - bi; ++bi; }
+    const int bj = bi + rem;
+    const double *ui[4], *uj[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      ui[r] = U + (int64_t)min(4 * bi + r, n - 1) * ld;
+      uj[r] = U + (int64_t)min(4 * bj + r, n - 1) * ld;
+    }
+    double acc[4][4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
+    for (int k = 0; k < n; ++k) {
+      double x[4], z[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) { x[r] = ui[r][k]; z[r] = uj[r][k]; }
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[r][c] = fma(x[r], z[c], acc[r][c]);
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int i = 4 * bi + r, j = 4 * bj + c;
+        if (i < j && j < n && acc[r][c] * acc[r][c] > c2 * nrm[i] * nrm[j]) bad = 1;
+      }
+  }
+  return !__syncthreads_or(bad);
+}
+
 // G lanes own one column pair (rows i = sub + G*c), 32/G pairs per warp.
 template <int G, int EPL, bool GU>
 __global__ void __launch_bounds__(512, 1) k_eig(EigArgs a) {
@@ -124,15 +204,7 @@ __global__ void __launch_bounds__(512, 1) k_eig(EigArgs a) {
     sched[e] = (unsigned short)(p | (q << 8));
   }
   // ---- 1. gather X_b (svec) into global, Frobenius norm -------------------------
-  double fro = 0.0;
-  for (int e = tid; e < L; e += nt) {
-    const int64_t J = off + e;
-    double aty = 0.0;
-    for (int64_t t = a.Atp[J]; t < a.Atp[J + 1]; ++t) aty += a.Atv[t] * a.y[a.Atr[t]];
-    const double xb = proj ? a.X[J] + sigma * (aty - a.C[J]) : a.C[J] - aty;
-    a.Xb_out[J] = xb;              // mode 1 uses Xb_out as scratch for C - A*y
-    fro += xb * xb;                // svec norm == Frobenius norm
-  }
+  double fro = gather_xb(a, off, L, tid, nt, sigma, proj);
   {
     double v1[1] = {fro};
     block_sum<1>(v1, red);
@@ -161,26 +233,32 @@ __global__ void __launch_bounds__(512, 1) k_eig(EigArgs a) {
     // column j of the new U = A v_j + s v_j; one warp per column, rows lane + 32c.
     // Without GU the result overwrites v_j in place (each column is read and written
     // by one warp only), then U := V.
+    // Two columns per warp pass (j, j + nwarps) for two independent FMA chains.
     double *dst = GU ? U : V;
-    for (int j = warp; j < n; j += nwarps) {
-      const double *vj = V + j * n;
-      double acc[8];
+    for (int j = warp; j < n; j += 2 * nwarps) {
+      const int j2 = j + nwarps < n ? j + nwarps : j;
+      const double *vj = V + j * n, *vj2 = V + j2 * n;
+      double acc[8], acc2[8];
 #pragma unroll
-      for (int c = 0; c < 8; ++c) acc[c] = 0.0;
+      for (int c = 0; c < 8; ++c) { acc[c] = 0.0; acc2[c] = 0.0; }
       for (int q = 0; q < n; ++q) {
-        const double vq = vj[q];
+        const double vq = vj[q], vq2 = vj2[q];
         const double *aq = Abuf + q * n;
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
           const int i = lane + 32 * c;
-          if (i < n) acc[c] += aq[i] * vq;
+          if (i < n) { const double x = aq[i]; acc[c] += x * vq; acc2[c] += x * vq2; }
         }
       }
       __syncwarp();
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         const int i = lane + 32 * c;
-        if (i < n) dst[j * n + i] = acc[c] + s * vj[i];
+        if (i < n) {
+          const double w = acc[c] + s * vj[i], w2 = acc2[c] + s * vj2[i];
+          dst[j * n + i] = w;
+          if (j2 != j) dst[j2 * n + i] = w2;
+        }
       }
     }
     if (!GU) U = V;
@@ -194,6 +272,7 @@ __global__ void __launch_bounds__(512, 1) k_eig(EigArgs a) {
   double *nrm = lamv;             // reuses the eigenvalue slot until step 4
   const double tol = fmax(a.tol, 4.0 * n * 2.220446049250313e-16);
   const double tol2 = tol * tol, quad2 = 1e-18;   // quad: sweep with max |cos| < 1e-9 is final
+  const double mid2 = 1e-12, gram2 = 1e-24;       // Gram exit: |cos| <= 1e-12 for every pair
   bool converged = false;
   int sweep = 0;
   for (; sweep < a.max_sweeps; ++sweep) {
@@ -205,7 +284,7 @@ __global__ void __launch_bounds__(512, 1) k_eig(EigArgs a) {
       if (lane == 0) nrm[j] = t;
     }
     __syncthreads();
-    int rotated = 0, big = 0;
+    int rotated = 0, big = 0, mid = 0;
     for (int r = 0; r < NP - 1; ++r) {
       for (int P0 = warp * PPW; P0 < H; P0 += nwarps * PPW) {
         const int P = P0 + grp;
@@ -235,6 +314,7 @@ __global__ void __launch_bounds__(512, 1) k_eig(EigArgs a) {
         if (valid && ga != 0.0 && g2a > tol2 * ab) {
           rotated = 1;
           if (g2a > quad2 * ab) big = 1;
+          if (g2a > mid2 * ab) mid = 1;
           // tan(theta) zeroing u_p.u_q: t = sign(d) g2 / (|d| + sqrt(d^2 + g2^2)),
           // d = be - al, g2 = 2 ga. t needs only ~1e-10 relative accuracy (it just has to
           // shrink u_p.u_q); (cs, sn) are exactly orthogonal to fp64 precision.
@@ -274,6 +354,13 @@ __global__ void __launch_bounds__(512, 1) k_eig(EigArgs a) {
     const int any_big = __syncthreads_or(big);
     const int any_rot = __syncthreads_or(rotated);
     if (!any_rot || !any_big) { converged = true; break; }
+    // Every rotation of this sweep had |cos| <= 1e-6: by quadratic convergence the
+    // columns are probably orthogonal to ~1e-12 already. Check that directly (a Gram
+    // product, ~1/10 of a sweep) instead of running a verifying sweep.
+    if (!__syncthreads_or(mid) && gram_orthogonal(U, n, n, nrm, gram2, tid, nt)) {
+      converged = true;
+      break;
+    }
   }
   if (tid == 0) {
     if (!converged) atomicCAS(&a.st->eig_fail, 0, bidx + 1);
@@ -413,15 +500,7 @@ __global__ void __cluster_dims__(kClusterEig, 1, 1) __launch_bounds__(512, 1) k_
   const double isq2 = 0.70710678118654752440;
   const bool proj = (a.mode == 0);
   // ---- 1. gather X_b (each CTA half of the svec entries), Frobenius norm -------------
-  double fro = 0.0;
-  for (int e = crank * nt + tid; e < L; e += kClusterEig * nt) {
-    const int64_t J = off + e;
-    double aty = 0.0;
-    for (int64_t t = a.Atp[J]; t < a.Atp[J + 1]; ++t) aty += a.Atv[t] * a.y[a.Atr[t]];
-    const double xb = proj ? a.X[J] + sigma * (aty - a.C[J]) : a.C[J] - aty;
-    a.Xb_out[J] = xb;
-    fro += xb * xb;
-  }
+  double fro = gather_xb(a, off, L, crank * nt + tid, kClusterEig * nt, sigma, proj);
   {
     double v1[1] = {fro};
     block_sum<1>(v1, red);

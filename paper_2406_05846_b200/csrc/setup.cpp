@@ -1,3 +1,5 @@
+#include <cstdlib>
+#include <cstdio>
 // Host setup of libstrom: SDP assembly/validation and the one-time factorisation
 // of eps I + AA* (eq:strom:gpu:cholesky).
 //
@@ -480,6 +482,16 @@ strom_status build_factor(const Sdp &s, double eps_rel, double eps_abs, Factor &
       const int qj = KPi[qi][t] + nL;
       if (qj >= S0) f.T0.row(si)[qj - S0] = KPv[qi][t];
     }
+  }
+  if (getenv("STROM_VERBOSE")) {
+    fprintf(stderr, "[strom] m=%d leaf=%d R=%d S=%d stages=%d unique dense=%zu:", m, nL, S0 - nL, nS, P,
+            f.uK.size());
+    for (size_t u = 0; u < f.uK.size(); ++u) {
+      int cnt = 0;
+      for (int k = 0; k < P; ++k) cnt += (f.stage_uid[k] == (int)u);
+      fprintf(stderr, " [n=%d w=%d x%d]", f.uK[u].rows, f.uB[u].cols, cnt);
+    }
+    fprintf(stderr, "\n");
   }
   return STROM_OK;
 }
