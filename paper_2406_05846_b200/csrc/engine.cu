@@ -4,13 +4,13 @@
 // Per iteration, all on one stream, captured in a CUDA graph:
 //   solve(r(AX^k, AS^k))          -> y_half         K-TRSV  (8 phase kernels)
 //   eig per size class            -> X_b, S^{k+1}    K-EIG   (A*y_half gather fused in)
-//   spmv A S^{k+1}                -> AS              K-SPMV
 //   solve(r(AX^k, AS^{k+1}))      -> y^{k+1}         K-TRSV
 //   update (A*y gather)           -> X^{k+1}, partials  K-FUSE
-//   spmv A X^{k+1}                -> AX, partials    K-SPMV/K-FUSE
-//   finalize                      -> eta, sigma policy, done flag
-// Step 1 needs A(X^k) and A(S^k) only, which the previous iteration produced, so
-// Step 1 costs no SpMV.
+//   spmv A X^{k+1}                -> AX, partials, then (last CTA) eta, sigma policy,
+//                                    done flag          K-SPMV/K-FUSE
+// The rows of A S enter the solves' right-hand sides as sparse row dots (A has ~2.5
+// nonzeros per row), so no A S pass is launched; Step 1 reuses A X^k of the previous
+// iteration.
 #include <cooperative_groups.h>
 #include <cublas_v2.h>
 #include <cuda_runtime.h>
@@ -47,7 +47,6 @@ namespace {
 
 constexpr int kWarp = 32;
 constexpr int kGemvChunk = 8;       // vectors per warp in the dedup GEMV
-constexpr int kRedThreads = 256;
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -75,8 +74,31 @@ __device__ __forceinline__ void block_sum(double (&v)[NV], double *scratch /* NV
   }
 }
 
+// sum_t val[t] x[idx[t]] over t in [ptr[i], ptr[i+1]), accumulated in t order; the
+// index/value loads of four terms are issued together so that their L2 round trips
+// overlap (the rows here have 1-12 terms: the chain of dependent loads is the cost).
+template <typename P>
+__device__ __forceinline__ double sparse_dot(const P *ptr, const int32_t *idx, const double *val,
+                                             const double *x, int64_t i) {
+  const int64_t t0 = ptr[i], t1 = ptr[i + 1];
+  double s = 0.0;
+  for (int64_t t = t0; t < t1; t += 4) {
+    double v[4], xv[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      v[k] = 0.0; xv[k] = 0.0;
+      if (t + k < t1) { v[k] = val[t + k]; xv[k] = x[idx[t + k]]; }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (t + k < t1) s += v[k] * xv[k];
+  }
+  return s;
+}
+
 __device__ __forceinline__ double rhs(const RhsArgs &a, double inv_sigma, int i) {
-  return (a.b[i] - a.ax[i]) * inv_sigma - a.as[i] + a.ac[i];
+  const double as = a.S ? sparse_dot(a.Arp, a.Aci, a.Av, a.S, i) : 0.0;
+  return (a.b[i] - a.ax[i]) * inv_sigma - as + a.ac[i];
 }
 
 // Warp dot product sum_{j in [lo,hi)} a[j] x[j], 4 independent loads in flight per lane.
@@ -123,7 +145,18 @@ __global__ void k_solve_p1(SolveDev d, RhsArgs ra, const DevState *st) {
   const double is = 1.0 / st->sigma;
   const int q = d.nL + qi;
   double s = rhs(ra, is, q);
-  for (int64_t t = d.G_ptr[qi]; t < d.G_ptr[qi + 1]; ++t) s -= d.G_val[t] * rhs(ra, is, d.G_col[t]);
+  const int64_t t0 = d.G_ptr[qi], t1 = d.G_ptr[qi + 1];
+  for (int64_t t = t0; t < t1; t += 4) {     // four leaf right-hand sides in flight
+    double g[4], r[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      g[k] = 0.0; r[k] = 0.0;
+      if (t + k < t1) { g[k] = d.G_val[t + k]; r[k] = rhs(ra, is, d.G_col[t + k]); }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (t + k < t1) s -= g[k] * r[k];
+  }
   d.u[q] = s;
 }
 
@@ -247,8 +280,18 @@ __global__ void k_solve_p7(SolveDev d, RhsArgs ra, double *y, const DevState *st
   const int g = d.leaf_group[l], g0 = d.gptr[g], gs = d.gptr[g + 1] - g0, a = l - g0;
   const double *Kinv = d.gKinv + d.goff[g] + (int64_t)a * gs;
   double s = 0.0;
-  for (int c = 0; c < gs; ++c) s += Kinv[c] * rhs(ra, is, g0 + c);
-  for (int64_t t = d.Gt_ptr[l]; t < d.Gt_ptr[l + 1]; ++t) s -= d.Gt_val[t] * y[d.Gt_col[t]];
+  for (int c0 = 0; c0 < gs; c0 += 4) {       // leaf groups have <= 4 rows: one pass
+    double kv[4], r[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      kv[k] = 0.0; r[k] = 0.0;
+      if (c0 + k < gs) { kv[k] = Kinv[c0 + k]; r[k] = rhs(ra, is, g0 + c0 + k); }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (c0 + k < gs) s += kv[k] * r[k];
+  }
+  s -= sparse_dot(d.Gt_ptr, d.Gt_col, d.Gt_val, y, l);
   y[l] = s;
 }
 
@@ -262,28 +305,39 @@ __global__ void k_spmv(int m, const int64_t *rp, const int32_t *ci, const double
   if (st && st->done) return;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= m) return;
-  double s = 0.0;
-  for (int64_t t = rp[i]; t < rp[i + 1]; ++t) s += v[t] * x[ci[t]];
-  y[i] = s;
+  y[i] = sparse_dot(rp, ci, v, x, i);
 }
 
-// AX = A X^{k+1}; partials ||AX - b||^2, <b, y>  (Step 4 residuals)
+// AX = A X^{k+1}; partials ||AX - b||^2, <b, y>  (Step 4 residuals).
+// The last CTA to finish (arrival ticket) reduces every CTA's partials and those of
+// k_update in a fixed order and runs finalize_state (no separate reduction launch).
+__device__ void finalize_state(const double *part_ax, int nax, const double *part_up, int nup, DevState *st);
 __global__ void k_spmv_ax(int m, const int64_t *rp, const int32_t *ci, const double *v, const double *x,
-                          double *ax, const double *b, const double *y, double *part, const DevState *st) {
+                          double *ax, const double *b, const double *y, double *part, const double *part_up,
+                          int nup, DevState *st) {
   if (st->done) return;
   __shared__ double red[2 * 32];
+  __shared__ int last;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   double acc[2] = {0.0, 0.0};
   if (i < m) {
-    double s = 0.0;
-    for (int64_t t = rp[i]; t < rp[i + 1]; ++t) s += v[t] * x[ci[t]];
+    const double s = sparse_dot(rp, ci, v, x, i);
     ax[i] = s;
     const double d = s - b[i];
     acc[0] = d * d;
     acc[1] = b[i] * y[i];
   }
   block_sum<2>(acc, red);
-  if (threadIdx.x == 0) { part[2 * blockIdx.x] = acc[0]; part[2 * blockIdx.x + 1] = acc[1]; }
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = acc[0]; part[2 * blockIdx.x + 1] = acc[1];
+    __threadfence();
+    last = (atomicAdd(&st->ticket, 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  finalize_state(part, (int)gridDim.x, part_up, nup, st);
+  if (threadIdx.x == 0) st->ticket = 0;
 }
 
 // Step 4: X^{k+1} = X + tau sigma (S + A*y - C) (eq:strom:sgsadmm:solve-X); partials
@@ -296,8 +350,7 @@ __global__ void k_update(int64_t n, const int64_t *Atp, const int32_t *Atr, cons
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
   if (j < n) {
-    double aty = 0.0;
-    for (int64_t t = Atp[j]; t < Atp[j + 1]; ++t) aty += Atv[t] * y[Atr[t]];
+    const double aty = sparse_dot(Atp, Atr, Atv, y, j);
     const double sigma = st->sigma, tau = st->tau;
     const double rd = S[j] + aty - C[j];
     const double xn = X[j] + tau * sigma * rd;
@@ -314,14 +367,16 @@ __global__ void k_update(int64_t n, const int64_t *Atp, const int32_t *Atr, cons
     for (int k = 0; k < 4; ++k) part[4 * blockIdx.x + k] = acc[k];
 }
 
-// eta, sigma policy (reading Q2), termination
-__global__ void k_finalize(const double *part_ax, int nax, const double *part_up, int nup, DevState *st) {
-  if (st->done) return;
+// eta, sigma policy (reading Q2), termination; run by the last CTA of
+// k_spmv_ax with all of its threads
+__device__ void finalize_state(const double *part_ax, int nax, const double *part_up, int nup, DevState *st) {
   __shared__ double red[6 * 32];
   double acc[6] = {0, 0, 0, 0, 0, 0};
-  for (int b = threadIdx.x; b < nax; b += blockDim.x) { acc[0] += part_ax[2 * b]; acc[1] += part_ax[2 * b + 1]; }
+  for (int b = threadIdx.x; b < nax; b += blockDim.x) {
+    acc[0] += __ldcg(part_ax + 2 * b); acc[1] += __ldcg(part_ax + 2 * b + 1);
+  }
   for (int b = threadIdx.x; b < nup; b += blockDim.x)
-    for (int k = 0; k < 4; ++k) acc[2 + k] += part_up[4 * b + k];
+    for (int k = 0; k < 4; ++k) acc[2 + k] += __ldcg(part_up + 4 * b + k);
   block_sum<6>(acc, red);
   if (threadIdx.x == 0) {
     const double eta_p = sqrt(acc[0]) / (1.0 + st->normb);
@@ -379,7 +434,7 @@ struct strom_admm {
   int64_t *Arp = nullptr; int32_t *Aci = nullptr; double *Av = nullptr;
   int64_t *Atp = nullptr; int32_t *Atr = nullptr; double *Atv = nullptr;
   double *C = nullptr, *X = nullptr, *S = nullptr, *Xb = nullptr;
-  double *y = nullptr, *yh = nullptr, *AX = nullptr, *AS = nullptr, *AC = nullptr, *b = nullptr;
+  double *y = nullptr, *yh = nullptr, *AX = nullptr, *AC = nullptr, *b = nullptr;
   double *zeros_m = nullptr, *tmp_m = nullptr, *tmp_m2 = nullptr;
   double *part_ax = nullptr, *part_up = nullptr;
   int nax = 0, nup = 0;
@@ -578,7 +633,7 @@ strom_status launch_eig(strom_admm *h, int mode, const double *yv, int &nl) {
 strom_status launch_iteration_A(strom_admm *h, int &nl_total) {
   int nl = 0;
   nl_total = 0;
-  RhsArgs ra{h->b, h->AX, h->AS, h->AC};
+  RhsArgs ra{h->b, h->AX, h->AC, h->Arp, h->Aci, h->Av, h->S};
   strom_status st;
   if ((st = launch_solve(h, ra, h->yh, nl)) != STROM_OK) return st;       // Step 1
   nl_total += nl;
@@ -609,23 +664,19 @@ strom_status launch_iteration_B(strom_admm *h, int &nl_total) {
   const int TB = 256;
   int nl = 0;
   nl_total = 0;
-  RhsArgs ra{h->b, h->AX, h->AS, h->AC};
+  RhsArgs ra{h->b, h->AX, h->AC, h->Arp, h->Aci, h->Av, h->S};
   strom_status st;
-  // Step 3: A S^{k+1}, then solve
-  mark(h, "spmv_AS");
-  k_spmv<<<(h->m + TB - 1) / TB, TB, 0, s>>>(h->m, h->Arp, h->Aci, h->Av, h->S, h->AS, h->st);
-  nl_total += 1;
+  // Step 3: solve with A S^{k+1} formed inside the right-hand side
   if ((st = launch_solve(h, ra, h->y, nl)) != STROM_OK) return st;
   nl_total += nl;
   // Step 4 + residual partials
   mark(h, "update_X");
   k_update<<<h->nup, TB, 0, s>>>(h->n, h->Atp, h->Atr, h->Atv, h->y, h->X, h->S, h->C, h->Xb, h->part_up, h->st);
   mark(h, "spmv_AX_resid");
-  k_spmv_ax<<<h->nax, TB, 0, s>>>(h->m, h->Arp, h->Aci, h->Av, h->X, h->AX, h->b, h->y, h->part_ax, h->st);
-  mark(h, "finalize");
-  k_finalize<<<1, kRedThreads, 0, s>>>(h->part_ax, h->nax, h->part_up, h->nup, h->st);
+  k_spmv_ax<<<h->nax, TB, 0, s>>>(h->m, h->Arp, h->Aci, h->Av, h->X, h->AX, h->b, h->y, h->part_ax,
+                                  h->part_up, h->nup, h->st);
   mark(h, nullptr);
-  nl_total += 3;
+  nl_total += 2;
   CK(cudaGetLastError());
   return STROM_OK;
 }
@@ -729,7 +780,6 @@ strom_status reset_state(strom_admm *h) {
 strom_status recompute_products(strom_admm *h) {
   const int TB = 256;
   k_spmv<<<(h->m + TB - 1) / TB, TB, 0, h->stream>>>(h->m, h->Arp, h->Aci, h->Av, h->X, h->AX, nullptr);
-  k_spmv<<<(h->m + TB - 1) / TB, TB, 0, h->stream>>>(h->m, h->Arp, h->Aci, h->Av, h->S, h->AS, nullptr);
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(h->stream));
   return STROM_OK;
@@ -984,7 +1034,7 @@ strom_status strom_admm_setup(strom_admm **out, const strom_sdp *sdp_h, const st
     return st;
   if ((st = h->alloc(h->X, s.n)) || (st = h->alloc(h->S, s.n)) || (st = h->alloc(h->Xb, s.n)) ||
       (st = h->alloc(h->y, m)) || (st = h->alloc(h->yh, m)) || (st = h->alloc(h->AX, m)) ||
-      (st = h->alloc(h->AS, m)) || (st = h->alloc(h->AC, m)) || (st = h->alloc(h->zeros_m, m)) ||
+      (st = h->alloc(h->AC, m)) || (st = h->alloc(h->zeros_m, m)) ||
       (st = h->alloc(h->tmp_m, std::max<int64_t>(m, s.n))) || (st = h->alloc(h->tmp_m2, std::max<int64_t>(m, s.n))) ||
       (st = h->alloc(h->st, 1)) || (st = h->alloc(h->lam_dev, s.nblocks)))
     return st;
@@ -994,7 +1044,6 @@ strom_status strom_admm_setup(strom_admm **out, const strom_sdp *sdp_h, const st
   CK(cudaMemset(h->y, 0, sizeof(double) * m));
   CK(cudaMemset(h->yh, 0, sizeof(double) * m));
   CK(cudaMemset(h->AX, 0, sizeof(double) * m));
-  CK(cudaMemset(h->AS, 0, sizeof(double) * m));
   CK(cudaMemset(h->zeros_m, 0, sizeof(double) * m));
   const int TB = 256;
   h->nax = (m + TB - 1) / TB;
@@ -1050,11 +1099,15 @@ strom_status strom_admm_setup(strom_admm **out, const strom_sdp *sdp_h, const st
   for (int u = 0; u < nu; ++u) {
     std::vector<int32_t> stg;
     for (int k = 0; k < F.P; ++k) if (F.stage_uid[k] == u && F.R_off[k + 1] > F.R_off[k]) stg.push_back(k);
+    // a factor used by one stage with long rows (the first clique's block of the large
+    // problems: 14K-18K rows) is streamed with a CTA per row (more bytes in flight)
+    static const int cta_rows = [] { const char *e = getenv("STROM_GEMV_CTA_ROWS"); return e ? atoi(e) : 2048; }();
+    const bool cta_path = stg.size() == 1 && cta_rows > 0 && un[u] >= cta_rows;
     for (size_t c0 = 0; c0 < stg.size(); c0 += kGemvChunk) {
       const int cnt = (int)std::min<size_t>(kGemvChunk, stg.size() - c0);
       const int li = (int)slist.size();
       for (int c = 0; c < cnt; ++c) slist.push_back(stg[c0 + c]);
-      for (int i = 0; i < un[u]; ++i) multi.push_back(GemvItem{u, i, li, cnt});   // warp per row
+      for (int i = 0; i < un[u]; ++i) (cta_path ? items : multi).push_back(GemvItem{u, i, li, cnt});   // warp per row
     }
   }
   h->nsingle = (int)items.size();
@@ -1447,7 +1500,7 @@ strom_status strom_debug_solve(strom_admm *h, const double *r, double *y) {
   const int32_t dn = ds.done;
   ds.sigma = 1.0; ds.done = 0;
   CK(h2d(h, h->st, &ds, sizeof(DevState)));
-  RhsArgs ra{h->tmp_m, h->zeros_m, h->zeros_m, h->zeros_m};
+  RhsArgs ra{h->tmp_m, h->zeros_m, h->zeros_m, h->Arp, h->Aci, h->Av, nullptr};
   int nl = 0;
   strom_status st = launch_solve(h, ra, h->tmp_m2, nl);
   if (st) return st;

@@ -19,15 +19,19 @@ struct DevState {          // scalars living on the device
   int32_t sigma_period;
   int32_t eig_warm_valid;  // 1 once every block has a stored eigenbasis
   unsigned long long eig_sweeps;   // diagnostic: Jacobi sweeps summed over blocks
+  uint32_t ticket;         // CTA arrival counter of the fused residual reduction
   double sigma_ratio, sigma_factor, sigma_min, sigma_max;
   // residuals of the latest completed iterate
   double eta_p, eta_d, eta_g, pobj, dobj, eta_x, sigma_used;
 };
 
-// r_i = (b_i - AX_i) / sigma - AS_i + AC_i : Step 1/3 right-hand side
-// (eq:strom:sgsadmm:solve-y1/-y2), formed on the fly by the solve phases.
+// r_i = (b_i - AX_i) / sigma - (A S)_i + AC_i : Step 1/3 right-hand side
+// (eq:strom:sgsadmm:solve-y1/-y2), formed on the fly by the solve phases; (A S)_i is a
+// sparse row dot with the current S (no separate A S pass), skipped when S is null.
 struct RhsArgs {
-  const double *b, *ax, *as, *ac;
+  const double *b, *ax, *ac;
+  const int64_t *Arp; const int32_t *Aci; const double *Av;
+  const double *S;
 };
 
 struct SolveDev {

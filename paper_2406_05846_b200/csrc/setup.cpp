@@ -491,7 +491,13 @@ strom_status build_factor(const Sdp &s, double eps_rel, double eps_abs, Factor &
       for (int k = 0; k < P; ++k) cnt += (f.stage_uid[k] == (int)u);
       fprintf(stderr, " [n=%d w=%d x%d]", f.uK[u].rows, f.uB[u].cols, cnt);
     }
-    fprintf(stderr, "\n");
+    int64_t gmax = 0, gtmax = 0, amax = 0;
+    for (int qi = 0; qi < nQ; ++qi) gmax = std::max<int64_t>(gmax, f.G_ptr[qi + 1] - f.G_ptr[qi]);
+    for (int l = 0; l < nL; ++l) gtmax = std::max<int64_t>(gtmax, f.Gt_ptr[l + 1] - f.Gt_ptr[l]);
+    for (int i = 0; i < m; ++i) amax = std::max<int64_t>(amax, s.rowptr[i + 1] - s.rowptr[i]);
+    fprintf(stderr, "\n[strom] G nnz %lld (max/row %lld, mean %.2f), G^T max/row %lld, A max/row %lld\n",
+            (long long)f.G_ptr[nQ], (long long)gmax, nQ ? (double)f.G_ptr[nQ] / nQ : 0.0, (long long)gtmax,
+            (long long)amax);
   }
   return STROM_OK;
 }
