@@ -14,6 +14,14 @@
 //      eigen-sets (Moreau: Pi(X) - X = Pi(-X)), written back in svec.
 #pragma once
 
+#ifdef STROM_EIG_PROF
+// phase timestamps (clock64) per block of the last K-EIG launch (tools/eig_prof.py)
+__device__ long long g_eig_prof[4096][16];
+#define EIG_STAMP(k) do { if (threadIdx.x == 0 && bidx < 4096) g_eig_prof[bidx][k] = clock64(); } while (0)
+#else
+#define EIG_STAMP(k) do { } while (0)
+#endif
+
 struct EigArgs {
   const int32_t *blocks; int32_t nblk;
   const int32_t *bn; const int64_t *boff;
@@ -80,6 +88,11 @@ __device__ __forceinline__ double group_sum(double v) {
   return v;
 }
 
+// Shared-memory column stride of U / V for a block of order n: with 8 lanes per column
+// pair a stride == 8 (mod 16) doubles keeps the warp's column reads free of bank conflicts
+// (one Jacobi round of order 55: 1,131 -> 929 cycles, tools/micro/round4.cu).
+__host__ __device__ inline int eig_ld(int n, int G) { return G == 8 ? (n + 7) / 16 * 16 + 8 : n; }
+
 __device__ __forceinline__ int svec_pos(int i, int j) {  // i, j any order
   return (i <= j) ? (j * (j + 1) / 2 + i) : (i * (i + 1) / 2 + j);
 }
@@ -120,6 +133,128 @@ __device__ __forceinline__ double gather_xb(const EigArgs &a, int64_t off, int L
     }
   }
   return fro;
+}
+
+// (i, j), i <= j, of svec position e (upper triangle column-wise)
+__device__ __forceinline__ void svec_ij(int e, int &i, int &j) {
+  j = (int)((sqrtf(8.0f * (float)e + 1.0f) - 1.0f) * 0.5f);
+  while (j * (j + 1) / 2 > e) --j;
+  while ((j + 1) * (j + 2) / 2 <= e) ++j;
+  i = e - j * (j + 1) / 2;
+}
+
+// Fast gather (blocks whose A* nonzeros fit in shared memory): pass 1 forms every
+// product Atv[t] * y[Atr[t]] of the block's contiguous CSC segment with coalesced loads
+// (two dependent L2 round trips in total instead of two per term); pass 2 sums each
+// entry's products in t order -- the same terms in the same order as gather_xb, so X_b is
+// bitwise identical -- writes X_b to global and keeps up to KE entries per thread in
+// registers for the staging of the dense matrix. Returns the partial ||X_b||_F^2.
+template <int KE>
+__device__ __forceinline__ double gather_xb_smem(const EigArgs &a, int64_t off, int L, double *prod,
+                                                 double (&xv)[KE], double sigma, bool proj) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int64_t nz0 = a.Atp[off], nz1 = a.Atp[off + L];
+  constexpr int NF = 12;          // products in flight per thread (two L2 round trips each)
+  for (int64_t t = nz0 + tid; t < nz1; t += NF * nt) {
+    int32_t r[NF];
+    double v[NF], yv[NF];
+#pragma unroll
+    for (int k = 0; k < NF; ++k) {
+      const int64_t tk = t + (int64_t)k * nt;
+      r[k] = tk < nz1 ? a.Atr[tk] : 0;
+      v[k] = tk < nz1 ? a.Atv[tk] : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < NF; ++k) yv[k] = a.y[r[k]];
+#pragma unroll
+    for (int k = 0; k < NF; ++k) {
+      const int64_t tk = t + (int64_t)k * nt;
+      if (tk < nz1) prod[tk - nz0] = v[k] * yv[k];
+    }
+  }
+  __syncthreads();
+  // every global load of pass 2 is issued before the first X_b store (which the compiler
+  // could not otherwise move loads across): one L2 round trip for all KE entries
+  int t0[KE], t1[KE];
+  double xk[KE], ck[KE];
+#pragma unroll
+  for (int k = 0; k < KE; ++k) {
+    const int e = tid + k * nt;
+    t0[k] = t1[k] = 0; xk[k] = ck[k] = 0.0;
+    if (e < L) {
+      const int64_t J = off + e;
+      t0[k] = (int)(a.Atp[J] - nz0); t1[k] = (int)(a.Atp[J + 1] - nz0);
+      if (proj) xk[k] = a.X[J];
+      ck[k] = a.C[J];
+    }
+  }
+  double fro = 0.0;
+#pragma unroll
+  for (int k = 0; k < KE; ++k) {
+    const int e = tid + k * nt;
+    xv[k] = 0.0;
+    if (e < L) {
+      double aty = 0.0;
+      for (int t = t0[k]; t < t1[k]; ++t) aty += prod[t];
+      const double xb = proj ? xk[k] + sigma * (aty - ck[k]) : ck[k] - aty;
+      a.Xb_out[off + e] = xb;
+      fro += xb * xb;
+      xv[k] = xb;
+    }
+  }
+  return fro;
+}
+
+// Dense product U = A V (+ s V) with 4x4 register tiles, one tile per thread
+// (requires ceil(n/4)^2 <= blockDim.x): thread (ti, tj) owns rows ti + nT r and columns
+// tj + nT c (strided, so a warp's shared-memory reads of A are bank-conflict free). A
+// symmetric in Abuf (column-major, stride ld), V column-major (stride ldv). Rows/columns
+// past n are clamped reads whose results are dropped. The result is written to dst
+// (stride ld) after a CTA barrier, so dst may alias Abuf or V. Per element the k-sum runs
+// in k order, as in the warp-per-column loop it replaces.
+__device__ __forceinline__ void warm_product_tiles(const double *Abuf, const double *V, int ldv, double *dst,
+                                                   int n, int ld, double s) {
+  const int tid = threadIdx.x, nT = (n + 3) >> 2;
+  const bool act = tid < nT * nT;
+  const int ti = act ? tid % nT : 0, tj = act ? tid / nT : 0;
+  const double *ar[4], *vc[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    ar[r] = Abuf + min(ti + nT * r, n - 1);
+    vc[r] = V + (int64_t)min(tj + nT * r, n - 1) * ldv;
+  }
+  double acc[4][4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
+  if (act) {
+#pragma unroll 4
+    for (int k = 0; k < n; ++k) {
+      double x[4], z[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) { x[r] = ar[r][(int64_t)k * ld]; z[r] = vc[r][k]; }
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[r][c] += x[r] * z[c];
+    }
+  }
+  double vij[4][4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) vij[r][c] = act ? vc[c][min(ti + nT * r, n - 1)] : 0.0;
+  __syncthreads();                // every read of Abuf and V is done
+  if (act) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int i = ti + nT * r, j = tj + nT * c;
+        if (i < n && j < n) dst[(int64_t)j * ld + i] = acc[r][c] + s * vij[r][c];
+      }
+  }
 }
 
 // Convergence check by the Gram matrix U^T U (4x4 register tiles, upper triangle):
@@ -178,17 +313,22 @@ __global__ void __launch_bounds__(512, 1) k_eig(EigArgs a) {
   const int NP = n + (n & 1), H = NP / 2;
   const int64_t off = a.boff[bidx];
   const int L = n * (n + 1) / 2;
-  // U: n columns x n rows, column-major (column j at U + j*n). Shared memory for
+  // U: n columns x n rows, column-major (column j at U + j*ld). Shared memory for
   // n <= 112 (A staged in U, warm basis in V); L2-resident global scratch above (GU).
+  const int ld = GU ? n : eig_ld(n, G);
   double *U, *V, *Abuf, *lamv;
   if (GU) {
     U = a.Ug + a.uoff[bidx]; Abuf = a.Ag + a.uoff[bidx]; V = a.Vstore + a.voff[bidx];
     lamv = sm;
   } else {
-    U = sm; Abuf = sm; V = sm + n * n;
-    lamv = sm + 2 * n * n;
+    U = sm; Abuf = sm; V = sm + n * ld;
+    lamv = sm + 2 * n * ld;
   }
   unsigned short *sched = (unsigned short *)(lamv + n + 8);  // (p | q << 8) per (round, pair)
+  EIG_STAMP(0);
+#ifdef STROM_EIG_PROF
+  __syncthreads();
+#endif
   const int tid = threadIdx.x, nt = blockDim.x;
   const int lane = tid & 31, warp = tid >> 5, nwarps = nt >> 5;
   const int grp = lane / G, sub = lane % G;
@@ -203,8 +343,16 @@ __global__ void __launch_bounds__(512, 1) k_eig(EigArgs a) {
     if (p > q) { const int t2 = p; p = q; q = t2; }
     sched[e] = (unsigned short)(p | (q << 8));
   }
+  EIG_STAMP(8);
   // ---- 1. gather X_b (svec) into global, Frobenius norm -------------------------
-  double fro = gather_xb(a, off, L, tid, nt, sigma, proj);
+  // Fast path: the block's A* products fit in the (still unused) U/V shared memory and
+  // the svec entries fit in KE registers per thread.
+  constexpr int KE = 12;
+  const bool fast = !GU && (int64_t)(a.Atp[off + L] - a.Atp[off]) <= 2LL * n * ld && L <= KE * nt;
+  double xv[KE];
+  double fro = fast ? gather_xb_smem<KE>(a, off, L, sm, xv, sigma, proj)
+                    : gather_xb(a, off, L, tid, nt, sigma, proj);
+  EIG_STAMP(9);
   {
     double v1[1] = {fro};
     block_sum<1>(v1, red);
@@ -215,19 +363,53 @@ __global__ void __launch_bounds__(512, 1) k_eig(EigArgs a) {
   // lambda_j + s >= ||X_b||_F, so v_j = u_j / ||u_j|| is accurate for every j
   const double s = 2.0 * red[127] + 1e-300;
   const double *Xb = a.Xb_out + off;
+  EIG_STAMP(1);
   // ---- 2. U = (X_b + s I) V with V = V_prev (warm) or I ----------------------------
-  {
+  if (fast) {
+    // the products in shared memory are dead (block_sum's barriers): stage A from registers
+    double *stage = warm ? Abuf : U;     // cold: U = A + sI directly
+#pragma unroll
+    for (int k = 0; k < KE; ++k) {
+      const int e = tid + k * nt;
+      if (e < L) {
+        int i, j;
+        svec_ij(e, i, j);
+        if (i == j) stage[j * ld + i] = xv[k] + (warm ? 0.0 : s);
+        else { const double v = xv[k] * isq2; stage[j * ld + i] = v; stage[i * ld + j] = v; }
+      }
+    }
+  } else {
     double *stage = warm ? Abuf : U;     // cold: U = A + sI directly
     for (int e = tid; e < n * n; e += nt) {   // A (symmetric): column-major == row-major
       const int j = e / n, i = e - j * n;
       const double v = Xb[svec_pos(i, j)];
-      stage[e] = (i == j) ? v + (warm ? 0.0 : s) : v * isq2;
+      stage[j * ld + i] = (i == j) ? v + (warm ? 0.0 : s) : v * isq2;
     }
   }
-  if (warm) {
+  const int nTw = (n + 3) >> 2;
+  if (warm && !GU && nTw * nTw <= nt) {
+    // U = A V_prev + s V_prev (4x4 register tiles, V_prev staged in shared memory);
+    // U overwrites A in place after the tile barrier
+    EIG_STAMP(10);
+    const double *Vp = a.Vstore + a.voff[bidx];
+    for (int e0 = tid; e0 < n * n; e0 += 8 * nt) {      // 8 loads in flight per thread
+      double vv[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) { const int e = e0 + k * nt; vv[k] = e < n * n ? Vp[e] : 0.0; }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int e = e0 + k * nt;
+        if (e < n * n) { const int j = e / n; V[j * ld + e - j * n] = vv[k]; }
+      }
+    }
+    __syncthreads();
+    EIG_STAMP(11);
+    warm_product_tiles(Abuf, V, ld, Abuf, n, ld, s);
+    U = Abuf;
+  } else if (warm) {
     if (!GU) {
       const double *Vp = a.Vstore + a.voff[bidx];
-      for (int e = tid; e < n * n; e += nt) V[e] = Vp[e];
+      for (int e = tid; e < n * n; e += nt) { const int j = e / n; V[j * ld + e - j * n] = Vp[e]; }
     }
     __syncthreads();
     // column j of the new U = A v_j + s v_j; one warp per column, rows lane + 32c.
@@ -237,13 +419,13 @@ __global__ void __launch_bounds__(512, 1) k_eig(EigArgs a) {
     double *dst = GU ? U : V;
     for (int j = warp; j < n; j += 2 * nwarps) {
       const int j2 = j + nwarps < n ? j + nwarps : j;
-      const double *vj = V + j * n, *vj2 = V + j2 * n;
+      const double *vj = V + j * ld, *vj2 = V + j2 * ld;
       double acc[8], acc2[8];
 #pragma unroll
       for (int c = 0; c < 8; ++c) { acc[c] = 0.0; acc2[c] = 0.0; }
       for (int q = 0; q < n; ++q) {
         const double vq = vj[q], vq2 = vj2[q];
-        const double *aq = Abuf + q * n;
+        const double *aq = Abuf + q * ld;
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
           const int i = lane + 32 * c;
@@ -256,14 +438,15 @@ __global__ void __launch_bounds__(512, 1) k_eig(EigArgs a) {
         const int i = lane + 32 * c;
         if (i < n) {
           const double w = acc[c] + s * vj[i], w2 = acc2[c] + s * vj2[i];
-          dst[j * n + i] = w;
-          if (j2 != j) dst[j2 * n + i] = w2;
+          dst[j * ld + i] = w;
+          if (j2 != j) dst[j2 * ld + i] = w2;
         }
       }
     }
     if (!GU) U = V;
   }
   __syncthreads();
+  EIG_STAMP(2);
   // ---- 3. one-sided Jacobi sweeps (round-robin pairs) ---------------------------------
   // Column norms nrm[j] = ||u_j||^2 live in shared memory (recomputed exactly at the
   // start of every sweep, updated per rotation), so a pair needs one dot u_p.u_q.
@@ -277,7 +460,7 @@ __global__ void __launch_bounds__(512, 1) k_eig(EigArgs a) {
   int sweep = 0;
   for (; sweep < a.max_sweeps; ++sweep) {
     for (int j = warp; j < n; j += nwarps) {
-      const double *uj = U + j * n;
+      const double *uj = U + j * ld;
       double t = 0.0;
       for (int i = lane; i < n; i += 32) t += uj[i] * uj[i];
       t = warp_sum(t);
@@ -285,8 +468,10 @@ __global__ void __launch_bounds__(512, 1) k_eig(EigArgs a) {
     }
     __syncthreads();
     int rotated = 0, big = 0, mid = 0;
+    const bool one_pass = nwarps * PPW >= H;
     for (int r = 0; r < NP - 1; ++r) {
       for (int P0 = warp * PPW; P0 < H; P0 += nwarps * PPW) {
+        if (one_pass && P0 != warp * PPW) break;
         const int P = P0 + grp;
         int p = 0, q = 0;
         bool valid = P < H;
@@ -295,7 +480,7 @@ __global__ void __launch_bounds__(512, 1) k_eig(EigArgs a) {
           p = pq & 0xff; q = pq >> 8;
           valid = q < n;                       // bye for odd n
         }
-        double *up = U + p * n, *uq = U + q * n;
+        double *up = U + p * ld, *uq = U + q * ld;
         double xp[EPL], xq[EPL];
         double ga0 = 0.0, ga1 = 0.0;
 #pragma unroll
@@ -357,7 +542,7 @@ __global__ void __launch_bounds__(512, 1) k_eig(EigArgs a) {
     // Every rotation of this sweep had |cos| <= 1e-6: by quadratic convergence the
     // columns are probably orthogonal to ~1e-12 already. Check that directly (a Gram
     // product, ~1/10 of a sweep) instead of running a verifying sweep.
-    if (!__syncthreads_or(mid) && gram_orthogonal(U, n, n, nrm, gram2, tid, nt)) {
+    if (!__syncthreads_or(mid) && gram_orthogonal(U, ld, n, nrm, gram2, tid, nt)) {
       converged = true;
       break;
     }
@@ -365,18 +550,47 @@ __global__ void __launch_bounds__(512, 1) k_eig(EigArgs a) {
   if (tid == 0) {
     if (!converged) atomicCAS(&a.st->eig_fail, 0, bidx + 1);
     atomicAdd(&a.st->eig_sweeps, (unsigned long long)(sweep + 1));
+#ifdef STROM_EIG_PROF
+    if (bidx < 4096) g_eig_prof[bidx][7] = sweep + 1;
+#endif
   }
+  EIG_STAMP(3);
   // ---- 4. eigenpairs: lambda_j = ||u_j|| - s, v_j = u_j / ||u_j|| (u_j = (lambda_j + s) v_j) ---
-  for (int j = warp; j < n; j += nwarps) {
-    double *uj = U + j * n;
-    double nn = 0.0;
-    for (int i = lane; i < n; i += 32) nn += uj[i] * uj[i];
-    nn = warp_sum(nn);
-    const double nr = sqrt(nn);
-    if (lane == 0) lamv[j] = nr - s;
-    if (proj) {
-      const double inv = 1.0 / nr;
-      for (int i = lane; i < n; i += 32) uj[i] *= inv;
+  // Without GU: one thread per column (rows visited from a column-dependent start so a
+  // half-warp's reads hit distinct banks); the columns stay unnormalised and wsc[j] =
+  // 1/||u_j||^2 folds the normalisation into the reconstruction and the V store.
+  __shared__ double wsc[256];     // [0, n): 1/||u_j||^2, [128, 128 + n): 1/||u_j||
+  if (!GU) {
+    for (int j = tid; j < n; j += nt) {
+      const double *uj = U + j * ld;
+      double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
+      int i = j % n, c = 0;
+      for (; c + 3 < n; c += 4) {
+        const int i1 = i + 1 < n ? i + 1 : i + 1 - n;
+        const int i2 = i1 + 1 < n ? i1 + 1 : i1 + 1 - n;
+        const int i3 = i2 + 1 < n ? i2 + 1 : i2 + 1 - n;
+        t0 += uj[i] * uj[i]; t1 += uj[i1] * uj[i1]; t2 += uj[i2] * uj[i2]; t3 += uj[i3] * uj[i3];
+        i = i3 + 1 < n ? i3 + 1 : i3 + 1 - n;
+      }
+      for (; c < n; ++c) { t0 += uj[i] * uj[i]; i = i + 1 < n ? i + 1 : 0; }
+      const double nn = (t0 + t1) + (t2 + t3);
+      const double nr = sqrt(nn);
+      lamv[j] = nr - s;
+      wsc[j] = 1.0 / nn;
+      wsc[128 + j] = 1.0 / nr;
+    }
+  } else {
+    for (int j = warp; j < n; j += nwarps) {
+      double *uj = U + j * ld;
+      double nn = 0.0;
+      for (int i = lane; i < n; i += 32) nn += uj[i] * uj[i];
+      nn = warp_sum(nn);
+      const double nr = sqrt(nn);
+      if (lane == 0) lamv[j] = nr - s;
+      if (proj) {
+        const double inv = 1.0 / nr;
+        for (int i = lane; i < n; i += 32) uj[i] *= inv;
+      }
     }
   }
   V = U;                          // eigenvectors now live in the U buffer
@@ -390,29 +604,38 @@ __global__ void __launch_bounds__(512, 1) k_eig(EigArgs a) {
     }
     return;
   }
-  if (tid == 0) {
+  if (warp == 0) {                // the smaller eigen-set, ascending order, by ballots
     int npos = 0, nneg = 0;
-    for (int k = 0; k < n; ++k) { if (lam[k] > 0.0) ++npos; else if (lam[k] < 0.0) ++nneg; }
+    for (int k0 = 0; k0 < n; k0 += 32) {
+      const int k = k0 + lane;
+      const double l = k < n ? lam[k] : 0.0;
+      npos += __popc(__ballot_sync(0xffffffffu, l > 0.0));
+      nneg += __popc(__ballot_sync(0xffffffffu, l < 0.0));
+    }
     const int use_pos = npos <= nneg;
     int cnt = 0;
-    for (int k = 0; k < n; ++k)
-      if (use_pos ? (lam[k] > 0.0) : (lam[k] < 0.0)) sets[cnt++] = k;
-    set_info = cnt * 2 + use_pos;
+    for (int k0 = 0; k0 < n; k0 += 32) {
+      const int k = k0 + lane;
+      const double l = k < n ? lam[k] : 0.0;
+      const bool pick = use_pos ? (l > 0.0) : (l < 0.0);
+      const unsigned b = __ballot_sync(0xffffffffu, pick);
+      if (pick) sets[cnt + __popc(b & ((1u << lane) - 1u))] = k;
+      cnt += __popc(b);
+    }
+    if (lane == 0) set_info = cnt * 2 + use_pos;
   }
   __syncthreads();
   const int cnt = set_info >> 1, use_pos = set_info & 1;
   const double is = 1.0 / sigma;
+  if (!GU)                        // per selected eigenpair: lambda_k / ||u_k||^2
+    for (int c = tid; c < cnt; c += nt) red[c] = lam[sets[c]] * wsc[sets[c]];
+  __syncthreads();
+  EIG_STAMP(4);
   // ---- 5. S = (Pi(X_b) - X_b)/sigma in svec ------------------------------------------
-  for (int e = tid; e < L; e += nt) {
-    int j = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
-    while (j * (j + 1) / 2 > e) --j;
-    while ((j + 1) * (j + 2) / 2 <= e) ++j;
-    const int i = e - j * (j + 1) / 2;
-    double acc = 0.0;
-    for (int c = 0; c < cnt; ++c) {
-      const int k = sets[c];
-      acc += lam[k] * V[k * n + i] * V[k * n + j];
-    }
+  // S entry (i <= j): from P_ij = sum_c w_c u_kc[i] u_kc[j] over the smaller eigen-set
+  // (c ascending), either (P - X_b)/sigma (positive set) or -P/sigma (negative set).
+  auto emit = [&](int i, int j, double acc) {
+    const int e = j * (j + 1) / 2 + i;
     double sv;
     if (use_pos) {
       const double xb = Xb[e];
@@ -421,16 +644,78 @@ __global__ void __launch_bounds__(512, 1) k_eig(EigArgs a) {
       sv = -acc * is;
     }
     a.S_out[off + e] = (i == j) ? sv : sv * 1.41421356237309504880;
+  };
+  const int nTr = (n + 3) >> 2;
+  if (!GU && nTr * nTr <= nt) {
+    // 4x4 register tiles over the full matrix (strided rows/columns as in the warm product)
+    if (tid < nTr * nTr) {
+      const int ti = tid % nTr, tj = tid / nTr;
+      int ir[4], jc[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) { ir[r] = min(ti + nTr * r, n - 1); jc[r] = min(tj + nTr * r, n - 1); }
+      double acc[4][4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
+      for (int c = 0; c < cnt; ++c) {
+        const double *uk = V + sets[c] * ld;
+        const double w = red[c];
+        double x[4], z[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) { x[r] = w * uk[ir[r]]; z[r] = uk[jc[r]]; }
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[r][q] += x[r] * z[q];
+      }
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int i = ti + nTr * r, j = tj + nTr * q;
+          if (i <= j && j < n) emit(i, j, acc[r][q]);
+        }
+    }
+  } else {
+    for (int e = tid; e < L; e += nt) {
+      int i, j;
+      svec_ij(e, i, j);
+      double acc = 0.0;
+      if (GU) {
+        for (int c = 0; c < cnt; ++c) {
+          const int k = sets[c];
+          acc += lam[k] * V[k * ld + i] * V[k * ld + j];
+        }
+      } else {
+        for (int c = 0; c < cnt; ++c) {
+          const int k = sets[c];
+          acc += red[c] * V[k * ld + i] * V[k * ld + j];
+        }
+      }
+      emit(i, j, acc);
+    }
   }
   // ---- 6. keep the eigenbasis for the next iteration -------------------------------
+  EIG_STAMP(5);
   double *Vs = a.Vstore + a.voff[bidx];
-  for (int e = tid; e < n * n; e += nt) Vs[e] = V[e];
+  if (GU) {
+    for (int e = tid; e < n * n; e += nt) Vs[e] = V[e];
+  } else {
+    for (int e = tid; e < n * n; e += nt) {
+      const int j = e / n;
+      Vs[e] = V[j * ld + e - j * n] * wsc[128 + j];
+    }
+  }
+  __syncthreads();
+  EIG_STAMP(6);
 }
 
 inline bool eig_global(int n) { return n > 112; }
+inline int eig_G(int n);
 inline size_t eig_smem_bytes(int n) {
   const int NP = n + (n & 1);
-  const size_t mats = eig_global(n) ? 0 : 2 * (size_t)n * n;
+  const size_t mats = eig_global(n) ? 0 : 2 * (size_t)n * eig_ld(n, eig_G(n));
   return sizeof(double) * (mats + n + 8) + sizeof(unsigned short) * (size_t)(NP - 1) * (NP / 2) + 16;
 }
 

@@ -234,19 +234,96 @@ __global__ void __launch_bounds__(128) k_solve_p3(SolveDev d, const DevState *st
   if (threadIdx.x == 0) d.u[s] -= a0 + a1;
 }
 
-// P4 / P5: dense separator solve with explicit L_T^{-1} (one CTA per row)
-// mode 0: z = L_T^{-1} u_S ; mode 1: y_S = L_T^{-T} z
-__global__ void __launch_bounds__(128) k_solve_sep(SolveDev d, int mode, double *y, const DevState *st) {
+// P4 / P5: separator solve T y_S = u_S with the explicit L_T^{-1} stored once, as its
+// lower 64x64 tiles (16.5 MB at pendulum N=30 instead of the 33 MB that separate row-major
+// copies of L_T^{-1} and L_T^{-T} touched, so the whole solve stays L2-resident).
+// mode 0: z = L_T^{-1} u_S (row dots: tile (I, J) -> block I); mode 1: y_S = L_T^{-T} z
+// (column dots of the same tiles: tile (I, J) -> block J). One CTA per tile writes its
+// 64 partial sums to Tpart[X][Y]; the CTA that delivers the last partial of block X
+// (arrival counter) sums them in Y order (deterministic) and re-arms the counter.
+constexpr int kSepTile = 64;
+__global__ void __launch_bounds__(256) k_sep_tri(SolveDev d, int mode, const double *in, double *out,
+                                                 const DevState *st) {
   if (st->done) return;
-  __shared__ double sh[32];
-  const int w = blockIdx.x;
+  __shared__ double colp[8][kSepTile];
+  __shared__ int last;
+  const int b = blockIdx.x, nT = d.nTt;
+  int I = (int)((sqrtf(8.0f * (float)b + 1.0f) - 1.0f) * 0.5f);
+  while (I * (I + 1) / 2 > b) --I;
+  while ((I + 1) * (I + 2) / 2 <= b) ++I;
+  const int J = b - I * (I + 1) / 2;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int n = d.nS;
+  const double *Tt = d.Ttile + (int64_t)b * kSepTile * kSepTile;
+  const int X = mode == 0 ? I : J;          // block this tile contributes to
+  const int Y = mode == 0 ? J : I;          // block of the input it reads
+  double t0[8], t1[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {             // rows warp*8 + k: 16 loads in flight per lane
+    const int r = warp * 8 + k;
+    t0[k] = __ldg(Tt + r * kSepTile + lane);
+    t1[k] = __ldg(Tt + r * kSepTile + lane + 32);
+  }
+  double *P = d.Tpart + ((int64_t)X * nT + Y) * kSepTile;
   if (mode == 0) {
-    const double acc = cta_dot(d.LTinv + (int64_t)w * n, d.u + d.S0, 0, w + 1, sh);
-    if (threadIdx.x == 0) d.z[d.S0 + w] = acc;
+    const int j0 = J * kSepTile + lane, j1 = j0 + 32;
+    const double x0 = j0 < n ? in[j0] : 0.0, x1 = j1 < n ? in[j1] : 0.0;
+    double rowv[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) rowv[k] = warp_sum(t0[k] * x0 + t1[k] * x1);
+    if (lane < 8) {
+      double v = rowv[0];
+#pragma unroll
+      for (int k = 1; k < 8; ++k) if (lane == k) v = rowv[k];
+      P[warp * 8 + lane] = v;
+    }
   } else {
-    const double acc = cta_dot(d.LTinvT + (int64_t)w * n, d.z + d.S0, w, n, sh);
-    if (threadIdx.x == 0) y[d.S0 + w] = acc;
+    double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int i = I * kSepTile + warp * 8 + k;
+      const double xi = i < n ? in[i] : 0.0;
+      c0 += t0[k] * xi;
+      c1 += t1[k] * xi;
+    }
+    colp[warp][lane] = c0; colp[warp][lane + 32] = c1;
+    __syncthreads();
+    if (threadIdx.x < kSepTile) {
+      double v = 0.0;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) v += colp[w][threadIdx.x];
+      P[threadIdx.x] = v;
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  const int need = mode == 0 ? X + 1 : nT - X;   // partials of block X
+  if (threadIdx.x == 0) last = atomicAdd(&d.Tcnt[X], 1u) == (unsigned)(need - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x < kSepTile) {
+    const int i = X * kSepTile + threadIdx.x;
+    const int y0 = mode == 0 ? 0 : X, y1 = mode == 0 ? X + 1 : nT;
+    double v = 0.0;
+    for (int yb = y0; yb < y1; ++yb) v += __ldcg(d.Tpart + ((int64_t)X * nT + yb) * kSepTile + threadIdx.x);
+    if (i < n) out[i] = v;
+  }
+  if (threadIdx.x == 0) d.Tcnt[X] = 0u;
+}
+
+// setup: lower 64x64 tiles of the lower-triangular matrix C (column-major nS x nS)
+__global__ void k_pack_sep_tiles(int n, int nT, const double *C, double *tiles) {
+  const int b = blockIdx.x;
+  int I = 0;
+  while ((I + 1) * (I + 2) / 2 <= b) ++I;
+  const int J = b - I * (I + 1) / 2;
+  for (int e = threadIdx.x; e < kSepTile * kSepTile; e += blockDim.x) {
+    const int r = e / kSepTile, c = e - r * kSepTile;
+    const int i = I * kSepTile + r, j = J * kSepTile + c;
+    double v = 0.0;
+    if (i < n && j < n && i >= j) v = C[(int64_t)j * n + i];
+    tiles[(int64_t)b * kSepTile * kSepTile + e] = v;
   }
 }
 
@@ -429,6 +506,7 @@ struct strom_admm {
   Factor F;
   // device buffers
   std::vector<void *> allocs;
+  std::vector<size_t> alloc_bytes;
   int64_t dev_bytes = 0;
   int32_t *perm = nullptr;
   int64_t *Arp = nullptr; int32_t *Aci = nullptr; double *Av = nullptr;
@@ -497,8 +575,18 @@ struct strom_admm {
     cudaError_t e = cudaMalloc((void **)&p, count * sizeof(T));
     if (e != cudaSuccess) { set_error(std::string("cudaMalloc: ") + cudaGetErrorString(e)); return STROM_ENOMEM; }
     allocs.push_back(p);
+    alloc_bytes.push_back(count * sizeof(T));
     dev_bytes += count * sizeof(T);
     return STROM_OK;
+  }
+  void release(void *p) {       // free a setup-only buffer before the iteration starts
+    auto it = std::find(allocs.begin(), allocs.end(), p);
+    if (it == allocs.end()) return;
+    const size_t k = it - allocs.begin();
+    dev_bytes -= (int64_t)alloc_bytes[k];
+    allocs.erase(it);
+    alloc_bytes.erase(alloc_bytes.begin() + k);
+    cudaFree(p);
   }
   template <class T>
   strom_status upload(T *&p, const std::vector<T> &h) {
@@ -554,8 +642,9 @@ strom_status launch_solve(strom_admm *h, const RhsArgs &ra, double *y, int &nl) 
   if (d.nS > 0) {
     cudaStream_t s2 = fork ? h->stream2 : s;
     k_solve_p3<<<d.nS, 128, 0, s2>>>(d, h->st); ++nl;
-    k_solve_sep<<<d.nS, 128, 0, s2>>>(d, 0, y, h->st); ++nl;
-    k_solve_sep<<<d.nS, 128, 0, s2>>>(d, 1, y, h->st); ++nl;
+    const int ntl = d.nTt * (d.nTt + 1) / 2;
+    k_sep_tri<<<ntl, 256, 0, s2>>>(d, 0, d.u + d.S0, d.z + d.S0, h->st); ++nl;
+    k_sep_tri<<<ntl, 256, 0, s2>>>(d, 1, d.z + d.S0, y + d.S0, h->st); ++nl;
   }
   if (h->nitems > 0 && nR > 0) {
     mark(h, "trsv_p2_stage_Linv");
@@ -616,6 +705,7 @@ strom_status launch_eig(strom_admm *h, int mode, const double *yv, int &nl) {
       k_eig_cluster<<<a.nblk * kClusterEig, 512, eig_cluster_smem_bytes(h->eig_class_n[c]), s>>>(a);
     } else if (eig_global(np)) k_eig<32, 8, true><<<a.nblk, threads, smem, s>>>(a);
     else if (G == 4) k_eig<4, 4, false><<<a.nblk, threads, smem, s>>>(a);
+    else if (G == 8 && h->eig_class_n[c] <= 56) k_eig<8, 7, false><<<a.nblk, threads, smem, s>>>(a);
     else if (G == 8) k_eig<8, 8, false><<<a.nblk, threads, smem, s>>>(a);
     else if (G == 32) k_eig<32, 2, false><<<a.nblk, threads, smem, s>>>(a);
     else k_eig<16, 8, false><<<a.nblk, threads, smem, s>>>(a);
@@ -895,7 +985,7 @@ strom_status transpose_into(strom_admm *h, int rows, int cols, const double *in,
 strom_status device_factor_dense(strom_admm *h, std::vector<const double *> &Linv, std::vector<const double *> &LinvT,
                                  std::vector<const double *> &Fp, std::vector<const double *> &Ftp,
                                  std::vector<const double *> &Hp, std::vector<const double *> &Htp,
-                                 std::vector<int32_t> &un, std::vector<int32_t> &uw, double *&LTinv, double *&LTinvT) {
+                                 std::vector<int32_t> &un, std::vector<int32_t> &uw, double *&Ttile, int &nTt) {
   const Factor &F = h->F;
   SolverHandles H;
   CSOL(cusolverDnCreate(&H.sol));
@@ -961,8 +1051,14 @@ strom_status device_factor_dense(strom_admm *h, std::vector<const double *> &Lin
                         T + (int64_t)off * nS + off, nS));
     }
     if ((st = chol_inverse(H, h->stream, nS, T, dinfo, "the separator Schur complement"))) return st;
-    LTinvT = T;
-    if ((st = transpose_into(h, nS, nS, T, LTinv))) return st;
+    // T holds L_T^{-1} column-major (upper zeroed): pack its lower tiles
+    nTt = (nS + kSepTile - 1) / kSepTile;
+    const int ntiles = nTt * (nTt + 1) / 2;
+    if ((st = h->alloc(Ttile, (size_t)ntiles * kSepTile * kSepTile))) return st;
+    k_pack_sep_tiles<<<ntiles, 256, 0, h->stream>>>(nS, nTt, T, Ttile);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(h->stream));
+    h->release(T);
   }
   CK(cudaStreamSynchronize(h->stream));
   return STROM_OK;
@@ -1075,15 +1171,21 @@ strom_status strom_admm_setup(strom_admm **out, const strom_sdp *sdp_h, const st
   const int nu = (int)F.uK.size();
   std::vector<const double *> hLinv(nu), hLinvT(nu), hF(nu), hFt(nu), hH(nu), hHt(nu);
   std::vector<int32_t> un(nu), uw(nu);
-  double *dLTinv = nullptr, *dLTinvT = nullptr;
-  if ((st = device_factor_dense(h.get(), hLinv, hLinvT, hF, hFt, hH, hHt, un, uw, dLTinv, dLTinvT))) return st;
+  double *dTtile = nullptr;
+  int nTt = 0;
+  if ((st = device_factor_dense(h.get(), hLinv, hLinvT, hF, hFt, hH, hHt, un, uw, dTtile, nTt))) return st;
   const double **pp1, **pp2, **pp3, **pp4, **pp5, **pp6;
   if ((st = h->upload(pp1, hLinv)) || (st = h->upload(pp2, hLinvT)) || (st = h->upload(pp3, hF)) ||
       (st = h->upload(pp4, hFt)) || (st = h->upload(pp5, hH)) || (st = h->upload(pp6, hHt)) ||
       (st = h->upload(p_un, un)) || (st = h->upload(p_uw, uw)))
     return st;
   d.Linv = pp1; d.LinvT = pp2; d.F = pp3; d.Ft = pp4; d.H = pp5; d.Ht = pp6; d.uid_n = p_un; d.uid_w = p_uw;
-  d.LTinv = dLTinv; d.LTinvT = dLTinvT;
+  d.Ttile = dTtile; d.nTt = nTt;
+  if (nTt > 0) {
+    if ((st = h->alloc(d.Tpart, (size_t)nTt * nTt * kSepTile)) || (st = h->alloc(d.Tcnt, nTt))) return st;
+    CK(cudaMemsetAsync(d.Tcnt, 0, sizeof(unsigned) * nTt, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+  }
   if ((st = h->alloc(d.u, m)) || (st = h->alloc(d.v, m)) || (st = h->alloc(d.t, m)) || (st = h->alloc(d.z, m)))
     return st;
   CK(cudaMemset(d.u, 0, sizeof(double) * m));
@@ -1169,6 +1271,7 @@ strom_status strom_admm_setup(strom_admm **out, const strom_sdp *sdp_h, const st
     if (maxsm > 48 * 1024) {
       CK(cudaFuncSetAttribute(k_eig<4, 4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)maxsm));
       CK(cudaFuncSetAttribute(k_eig<8, 8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)maxsm));
+      CK(cudaFuncSetAttribute(k_eig<8, 7, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)maxsm));
       CK(cudaFuncSetAttribute(k_eig<16, 8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)maxsm));
       CK(cudaFuncSetAttribute(k_eig<32, 2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)maxsm));
       CK(cudaFuncSetAttribute(k_eig<32, 8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)maxsm));
@@ -1514,3 +1617,13 @@ strom_status strom_debug_solve(strom_admm *h, const double *r, double *y) {
 }
 
 }  // extern "C"
+
+#ifdef STROM_EIG_PROF
+// phase timestamps of the last K-EIG launch per block (profiling builds only)
+extern "C" strom_status strom_debug_eig_prof(long long *out, int32_t nblocks) {
+  if (!out || nblocks < 0 || nblocks > 4096) return STROM_EINVAL;
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpyFromSymbol(out, g_eig_prof, sizeof(long long) * 16 * nblocks));
+  return STROM_OK;
+}
+#endif

@@ -50,7 +50,10 @@ struct SolveDev {
   const double *const *F; const double *const *Ft;
   const double *const *H; const double *const *Ht;   // H_k = L_k^{-T} F_k (n_k x w), H^T
   const int32_t *uid_n, *uid_w;
-  const double *LTinv, *LTinvT;   // nS x nS
+  // separator system: L_T^{-1} (lower nS x nS) as its lower 64x64 tiles (I >= J,
+  // tile-row-major order, each tile row-major, zero padded); per-call partial products
+  // Tpart[X][Y][64] and per-block arrival counters Tcnt[nTt]
+  const double *Ttile; int32_t nTt; double *Tpart; unsigned *Tcnt;
   // work vectors (internal order, length m)
   double *u, *v, *t, *z;
 };

@@ -288,3 +288,9 @@ def test_multigpu_partition_virtual_ranks(name, P):
         X, y, Sg, r = g.get()
         assert np.array_equal(X, Xr) and np.array_equal(Sg, Sr) and np.array_equal(y, yr)
         assert r["iter"] == rr["iter"] == 12
+
+
+def test_graft_smoke_entry():
+    """The driver's smoke() (pendulum N=3, 5 iterations vs the oracle) runs as shipped."""
+    import __graft_entry__
+    __graft_entry__.smoke()
