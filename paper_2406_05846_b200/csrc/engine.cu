@@ -96,9 +96,11 @@ __device__ __forceinline__ double sparse_dot(const P *ptr, const int32_t *idx, c
   return s;
 }
 
-__device__ __forceinline__ double rhs(const RhsArgs &a, double inv_sigma, int i) {
-  const double as = a.S ? sparse_dot(a.Arp, a.Aci, a.Av, a.S, i) : 0.0;
-  return (a.b[i] - a.ax[i]) * inv_sigma - as + a.ac[i];
+// right-hand side of row i; wi = AC_i - (A S)_i (cached in a.w when usew)
+__device__ __forceinline__ double rhs(const RhsArgs &a, double inv_sigma, int i, bool usew, double &wi) {
+  if (usew) wi = a.w[i];
+  else wi = a.ac[i] - (a.S ? sparse_dot(a.Arp, a.Aci, a.Av, a.S, i) : 0.0);
+  return (a.b[i] - a.ax[i]) * inv_sigma + wi;
 }
 
 // Warp dot product sum_{j in [lo,hi)} a[j] x[j], 4 independent loads in flight per lane.
@@ -143,15 +145,18 @@ __global__ void k_solve_p1(SolveDev d, RhsArgs ra, const DevState *st) {
   const int qi = blockIdx.x * blockDim.x + threadIdx.x;
   if (qi >= d.nQ) return;
   const double is = 1.0 / st->sigma;
+  const bool usew = ra.w && st->w_valid;
   const int q = d.nL + qi;
-  double s = rhs(ra, is, q);
+  double wq;
+  double s = rhs(ra, is, q, usew, wq);
+  if (ra.wout) ra.wout[q] = wq;
   const int64_t t0 = d.G_ptr[qi], t1 = d.G_ptr[qi + 1];
   for (int64_t t = t0; t < t1; t += 4) {     // four leaf right-hand sides in flight
-    double g[4], r[4];
+    double g[4], r[4], wl;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       g[k] = 0.0; r[k] = 0.0;
-      if (t + k < t1) { g[k] = d.G_val[t + k]; r[k] = rhs(ra, is, d.G_col[t + k]); }
+      if (t + k < t1) { g[k] = d.G_val[t + k]; r[k] = rhs(ra, is, d.G_col[t + k], usew, wl); }
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k)
@@ -218,20 +223,24 @@ __global__ void __launch_bounds__(256) k_gemv_stage(SolveDev d, const GemvItem *
 }
 
 // P3: u_S -= sum_k F_k^T v_k = sum_k H_k^T u_Rk  (H_k = L_k^{-T} F_k, so it needs only P1's
-// output and runs concurrently with P2; one CTA per separator row, in place on u)
-__global__ void __launch_bounds__(128) k_solve_p3(SolveDev d, const DevState *st) {
+// output and runs concurrently with P2). One warp per separator row (grid-stride over a
+// few CTAs per SM: the row dots are short, CTA dispatch was the cost), in place on u.
+__global__ void __launch_bounds__(256) k_solve_p3(SolveDev d, const DevState *st) {
   if (st->done) return;
-  __shared__ double sh[32];
-  const int s = d.S0 + blockIdx.x;
-  int j = 0;
-  while (j + 1 < d.P - 1 && d.S_off[j + 1] <= s) ++j;   // separator block of s
-  const int c = s - d.S_off[j];
-  // stage j: its right separator is S_j -> column wl_j + c; stage j+1: left -> column c
-  const int u0 = d.stage_uid[j], n0 = d.uid_n[u0];
-  const int u1 = d.stage_uid[j + 1], n1 = d.uid_n[u1];
-  const double a0 = cta_dot(d.Ht[u0] + (int64_t)(d.stage_wl[j] + c) * n0, d.u + d.R_off[j], 0, n0, sh);
-  const double a1 = cta_dot(d.Ht[u1] + (int64_t)c * n1, d.u + d.R_off[j + 1], 0, n1, sh);
-  if (threadIdx.x == 0) d.u[s] -= a0 + a1;
+  const int lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < d.nS; w += nw) {
+    const int s = d.S0 + w;
+    int j = 0;
+    while (j + 1 < d.P - 1 && d.S_off[j + 1] <= s) ++j;   // separator block of s
+    const int c = s - d.S_off[j];
+    // stage j: its right separator is S_j -> column wl_j + c; stage j+1: left -> column c
+    const int u0 = d.stage_uid[j], n0 = d.uid_n[u0];
+    const int u1 = d.stage_uid[j + 1], n1 = d.uid_n[u1];
+    const double a0 = warp_dot(d.Ht[u0] + (int64_t)(d.stage_wl[j] + c) * n0, d.u + d.R_off[j], 0, n0, lane);
+    const double a1 = warp_dot(d.Ht[u1] + (int64_t)c * n1, d.u + d.R_off[j + 1], 0, n1, lane);
+    if (lane == 0) d.u[s] -= a0 + a1;
+  }
 }
 
 // P4 / P5: separator solve T y_S = u_S with the explicit L_T^{-1} stored once, as its
@@ -331,9 +340,9 @@ __global__ void k_pack_sep_tiles(int n, int nT, const double *C, double *tiles) 
 // (warp per interior row)
 __global__ void k_solve_p6a(SolveDev d, const int32_t *row_stage, double *y, const DevState *st) {
   if (st->done) return;
-  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, nw = (gridDim.x * blockDim.x) >> 5;
   const int nR = d.S0 - d.nL;
-  if (w >= nR) return;
+  for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nR; w += nw) {
   const int q = d.nL + w;
   const int k = row_stage[w];
   const int uid = d.stage_uid[k], wk = d.uid_w[uid], wl = d.stage_wl[k];
@@ -346,6 +355,7 @@ __global__ void k_solve_p6a(SolveDev d, const int32_t *row_stage, double *y, con
   }
   acc = warp_sum(acc);
   if (lane == 0) y[q] = d.t[q] - acc;
+  }
 }
 
 // P7: y_L = K_LL^{-1} r_L - G^T y_Q   (thread per leaf row)
@@ -354,6 +364,7 @@ __global__ void k_solve_p7(SolveDev d, RhsArgs ra, double *y, const DevState *st
   const int l = blockIdx.x * blockDim.x + threadIdx.x;
   if (l >= d.nL) return;
   const double is = 1.0 / st->sigma;
+  const bool usew = ra.w && st->w_valid;
   const int g = d.leaf_group[l], g0 = d.gptr[g], gs = d.gptr[g + 1] - g0, a = l - g0;
   const double *Kinv = d.gKinv + d.goff[g] + (int64_t)a * gs;
   double s = 0.0;
@@ -362,7 +373,12 @@ __global__ void k_solve_p7(SolveDev d, RhsArgs ra, double *y, const DevState *st
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       kv[k] = 0.0; r[k] = 0.0;
-      if (c0 + k < gs) { kv[k] = Kinv[c0 + k]; r[k] = rhs(ra, is, g0 + c0 + k); }
+      if (c0 + k < gs) {
+        double wk;
+        kv[k] = Kinv[c0 + k];
+        r[k] = rhs(ra, is, g0 + c0 + k, usew, wk);
+        if (ra.wout && c0 + k == a) ra.wout[l] = wk;   // this thread's own leaf row
+      }
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k)
@@ -474,6 +490,7 @@ __device__ void finalize_state(const double *part_ax, int nax, const double *par
     }
     const double eta = fmax(eta_p, fmax(eta_d, eta_g));
     st->eig_warm_valid = 1;   // every block's eigenbasis was stored by this iteration
+    st->w_valid = 1;          // Step 3 stored AC - A S^{k+1} for every row
     if ((st->tol >= 0.0 && eta <= st->tol) || st->nan_flag) st->done = 1;
   }
 }
@@ -514,6 +531,7 @@ struct strom_admm {
   double *C = nullptr, *X = nullptr, *S = nullptr, *Xb = nullptr;
   double *y = nullptr, *yh = nullptr, *AX = nullptr, *AC = nullptr, *b = nullptr;
   double *zeros_m = nullptr, *tmp_m = nullptr, *tmp_m2 = nullptr;
+  double *wrhs = nullptr;      // AC - A S^{k+1} from Step 3, reused by the next Step 1
   double *part_ax = nullptr, *part_up = nullptr;
   int nax = 0, nup = 0;
   int32_t *bn = nullptr; int64_t *boff = nullptr;
@@ -543,6 +561,7 @@ struct strom_admm {
   cudaGraphExec_t execK = nullptr, exec1 = nullptr;
   int K = 50;
   int launches_per_iter = 0;
+  int num_sms = 148;
   double *lam_dev = nullptr;
   double *Vstore = nullptr; int64_t *voff = nullptr;
   double *Ug = nullptr, *Ag = nullptr; int64_t *uoff = nullptr;
@@ -641,7 +660,7 @@ strom_status launch_solve(strom_admm *h, const RhsArgs &ra, double *y, int &nl) 
   }
   if (d.nS > 0) {
     cudaStream_t s2 = fork ? h->stream2 : s;
-    k_solve_p3<<<d.nS, 128, 0, s2>>>(d, h->st); ++nl;
+    k_solve_p3<<<std::min((d.nS + 7) / 8, 4 * h->num_sms), 256, 0, s2>>>(d, h->st); ++nl;
     const int ntl = d.nTt * (d.nTt + 1) / 2;
     k_sep_tri<<<ntl, 256, 0, s2>>>(d, 0, d.u + d.S0, d.z + d.S0, h->st); ++nl;
     k_sep_tri<<<ntl, 256, 0, s2>>>(d, 1, d.z + d.S0, y + d.S0, h->st); ++nl;
@@ -661,7 +680,7 @@ strom_status launch_solve(strom_admm *h, const RhsArgs &ra, double *y, int &nl) 
   }
   if (nR > 0 && d.nS > 0) {
     mark(h, "trsv_p6a_stage_H");
-    k_solve_p6a<<<(nR * 32 + TB - 1) / TB, TB, 0, s>>>(d, h->row_stage_R, y, h->st); ++nl;
+    k_solve_p6a<<<std::min((nR * 32 + TB - 1) / TB, 8 * h->num_sms), TB, 0, s>>>(d, h->row_stage_R, y, h->st); ++nl;
   }
   if (d.nL > 0) { mark(h, "trsv_p7_leaf_bwd"); k_solve_p7<<<(d.nL + TB - 1) / TB, TB, 0, s>>>(d, ra, y, h->st); ++nl; }
   CK(cudaGetLastError());
@@ -723,7 +742,7 @@ strom_status launch_eig(strom_admm *h, int mode, const double *yv, int &nl) {
 strom_status launch_iteration_A(strom_admm *h, int &nl_total) {
   int nl = 0;
   nl_total = 0;
-  RhsArgs ra{h->b, h->AX, h->AC, h->Arp, h->Aci, h->Av, h->S};
+  RhsArgs ra{h->b, h->AX, h->AC, h->Arp, h->Aci, h->Av, h->S, h->wrhs, nullptr};
   strom_status st;
   if ((st = launch_solve(h, ra, h->yh, nl)) != STROM_OK) return st;       // Step 1
   nl_total += nl;
@@ -754,9 +773,9 @@ strom_status launch_iteration_B(strom_admm *h, int &nl_total) {
   const int TB = 256;
   int nl = 0;
   nl_total = 0;
-  RhsArgs ra{h->b, h->AX, h->AC, h->Arp, h->Aci, h->Av, h->S};
+  RhsArgs ra{h->b, h->AX, h->AC, h->Arp, h->Aci, h->Av, h->S, nullptr, h->wrhs};
   strom_status st;
-  // Step 3: solve with A S^{k+1} formed inside the right-hand side
+  // Step 3: solve with A S^{k+1} formed inside the right-hand side (and kept in wrhs)
   if ((st = launch_solve(h, ra, h->y, nl)) != STROM_OK) return st;
   nl_total += nl;
   // Step 4 + residual partials
@@ -1097,6 +1116,7 @@ strom_status strom_admm_setup(strom_admm **out, const strom_sdp *sdp_h, const st
   strom_status st = build_factor(s, cfg->eps_rel, cfg->eps, h->F);
   if (st != STROM_OK) return st;
   CK(cudaSetDevice(device));
+  CK(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device));
   if (cuda_stream) h->stream = (cudaStream_t)cuda_stream;
   else { CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking)); h->own_stream = true; }
   const Factor &F = h->F;
@@ -1130,7 +1150,7 @@ strom_status strom_admm_setup(strom_admm **out, const strom_sdp *sdp_h, const st
     return st;
   if ((st = h->alloc(h->X, s.n)) || (st = h->alloc(h->S, s.n)) || (st = h->alloc(h->Xb, s.n)) ||
       (st = h->alloc(h->y, m)) || (st = h->alloc(h->yh, m)) || (st = h->alloc(h->AX, m)) ||
-      (st = h->alloc(h->AC, m)) || (st = h->alloc(h->zeros_m, m)) ||
+      (st = h->alloc(h->AC, m)) || (st = h->alloc(h->zeros_m, m)) || (st = h->alloc(h->wrhs, m)) ||
       (st = h->alloc(h->tmp_m, std::max<int64_t>(m, s.n))) || (st = h->alloc(h->tmp_m2, std::max<int64_t>(m, s.n))) ||
       (st = h->alloc(h->st, 1)) || (st = h->alloc(h->lam_dev, s.nblocks)))
     return st;
@@ -1558,6 +1578,7 @@ strom_status strom_debug_project_psd(strom_admm *h, const double *Xb, double sig
   CK(d2h(h, &ds, h->st, sizeof(DevState)));
   const int32_t fail = ds.eig_fail;
   ds.sigma = sg_old; ds.done = done_old; ds.eig_fail = 0; ds.eig_warm_valid = warm_old;
+  ds.w_valid = 0;                 // S was overwritten
   CK(h2d(h, h->st, &ds, sizeof(DevState)));
   // restore S of the iterate is not needed for tests (they reset with set_start)
   if (fail) { set_error("Jacobi sweep cap reached"); return STROM_EEIG; }
@@ -1603,7 +1624,7 @@ strom_status strom_debug_solve(strom_admm *h, const double *r, double *y) {
   const int32_t dn = ds.done;
   ds.sigma = 1.0; ds.done = 0;
   CK(h2d(h, h->st, &ds, sizeof(DevState)));
-  RhsArgs ra{h->tmp_m, h->zeros_m, h->zeros_m, h->Arp, h->Aci, h->Av, nullptr};
+  RhsArgs ra{h->tmp_m, h->zeros_m, h->zeros_m, h->Arp, h->Aci, h->Av, nullptr, nullptr, nullptr};
   int nl = 0;
   strom_status st = launch_solve(h, ra, h->tmp_m2, nl);
   if (st) return st;

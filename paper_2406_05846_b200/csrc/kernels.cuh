@@ -18,6 +18,7 @@ struct DevState {          // scalars living on the device
   int32_t nan_flag;
   int32_t sigma_period;
   int32_t eig_warm_valid;  // 1 once every block has a stored eigenbasis
+  int32_t w_valid;         // 1 when RhsArgs::w holds AC - A S for the current S
   unsigned long long eig_sweeps;   // diagnostic: Jacobi sweeps summed over blocks
   uint32_t ticket;         // CTA arrival counter of the fused residual reduction
   double sigma_ratio, sigma_factor, sigma_min, sigma_max;
@@ -25,13 +26,17 @@ struct DevState {          // scalars living on the device
   double eta_p, eta_d, eta_g, pobj, dobj, eta_x, sigma_used;
 };
 
-// r_i = (b_i - AX_i) / sigma - (A S)_i + AC_i : Step 1/3 right-hand side
+// r_i = (b_i - AX_i) / sigma + (AC_i - (A S)_i) : Step 1/3 right-hand side
 // (eq:strom:sgsadmm:solve-y1/-y2), formed on the fly by the solve phases; (A S)_i is a
 // sparse row dot with the current S (no separate A S pass), skipped when S is null.
+// Step 3 stores w_i = AC_i - (A S^{k+1})_i for every row it forms (wout); Step 1 of the
+// next iteration has the same S and reads w instead of re-forming the dots (w, when
+// DevState::w_valid).
 struct RhsArgs {
   const double *b, *ax, *ac;
   const int64_t *Arp; const int32_t *Aci; const double *Av;
   const double *S;
+  const double *w; double *wout;
 };
 
 struct SolveDev {
