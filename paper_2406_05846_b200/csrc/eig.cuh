@@ -302,7 +302,7 @@ __device__ __forceinline__ bool gram_orthogonal(const double *U, int ld, int n, 
 // G lanes own one column pair (rows i = sub + G*c), 32/G pairs per warp.
 template <int G, int EPL, bool GU>
 __global__ void __launch_bounds__(512, 1) k_eig(EigArgs a) {
-  if (a.st->done) return;
+  pdl_trigger();                  // static prologue below overlaps the previous kernel
   extern __shared__ double sm[];
   __shared__ double red[4 * 32];
   __shared__ int sets[128];
@@ -332,17 +332,19 @@ __global__ void __launch_bounds__(512, 1) k_eig(EigArgs a) {
   const int tid = threadIdx.x, nt = blockDim.x;
   const int lane = tid & 31, warp = tid >> 5, nwarps = nt >> 5;
   const int grp = lane / G, sub = lane % G;
-  const double sigma = a.st->sigma;
   const double isq2 = 0.70710678118654752440;
   const bool proj = (a.mode == 0);
-  const bool warm = proj && a.warm_enable && a.st->eig_warm_valid &&
-                    (a.cold_every <= 0 || (a.st->iter % a.cold_every) != 0);
   for (int e = tid; e < (NP - 1) * H; e += nt) {
     const int r = e / H, P = e - r * H;
     int p = rr_pos(P, r, NP - 1), q = rr_pos(NP - 1 - P, r, NP - 1);
     if (p > q) { const int t2 = p; p = q; q = t2; }
     sched[e] = (unsigned short)(p | (q << 8));
   }
+  pdl_wait();                     // everything below may read the previous kernels' output
+  if (a.st->done) return;
+  const double sigma = a.st->sigma;
+  const bool warm = proj && a.warm_enable && a.st->eig_warm_valid &&
+                    (a.cold_every <= 0 || (a.st->iter % a.cold_every) != 0);
   EIG_STAMP(8);
   // ---- 1. gather X_b (svec) into global, Frobenius norm -------------------------
   // Fast path: the block's A* products fit in the (still unused) U/V shared memory and
@@ -468,73 +470,75 @@ __global__ void __launch_bounds__(512, 1) k_eig(EigArgs a) {
     }
     __syncthreads();
     int rotated = 0, big = 0, mid = 0;
-    const bool one_pass = nwarps * PPW >= H;
-    for (int r = 0; r < NP - 1; ++r) {
-      for (int P0 = warp * PPW; P0 < H; P0 += nwarps * PPW) {
-        if (one_pass && P0 != warp * PPW) break;
-        const int P = P0 + grp;
-        int p = 0, q = 0;
-        bool valid = P < H;
-        if (valid) {
-          const unsigned pq = sched[r * H + P];
-          p = pq & 0xff; q = pq >> 8;
-          valid = q < n;                       // bye for odd n
-        }
-        double *up = U + p * ld, *uq = U + q * ld;
-        double xp[EPL], xq[EPL];
-        double ga0 = 0.0, ga1 = 0.0;
+    // One round: the G lanes of group `grp` own pair P of the round's schedule.
+    auto pair_step = [&](int r, int P) {
+      int p = 0, q = 0;
+      bool valid = P < H;
+      if (valid) {
+        const unsigned pq = sched[r * H + P];
+        p = pq & 0xff; q = pq >> 8;
+        valid = q < n;                         // bye for odd n
+      }
+      const double al = valid ? nrm[p] : 1.0, be = valid ? nrm[q] : 1.0;   // off the dot's chain
+      double *up = U + p * ld, *uq = U + q * ld;
+      double xp[EPL], xq[EPL];
+      double ga0 = 0.0, ga1 = 0.0;
+#pragma unroll
+      for (int c = 0; c < EPL; ++c) {
+        const int i = sub + G * c;
+        const bool ok = valid && i < n;
+        xp[c] = ok ? up[i] : 0.0;
+        xq[c] = ok ? uq[i] : 0.0;
+        if (c & 1) ga1 += xp[c] * xq[c]; else ga0 += xp[c] * xq[c];
+      }
+      double ga = ga0 + ga1;
+#pragma unroll
+      for (int o = G / 2; o > 0; o >>= 1) ga += __shfl_xor_sync(0xffffffffu, ga, o);
+      const double ab = al * be, g2a = ga * ga;
+      if (valid && ga != 0.0 && g2a > tol2 * ab) {
+        rotated = 1;
+        if (g2a > quad2 * ab) big = 1;
+        if (g2a > mid2 * ab) mid = 1;
+        // tan(theta) zeroing u_p.u_q: t = sign(d) g2 / (|d| + sqrt(d^2 + g2^2)),
+        // d = be - al, g2 = 2 ga. t needs only ~1e-10 relative accuracy (it just has to
+        // shrink u_p.u_q); (cs, sn) are exactly orthogonal to fp64 precision:
+        // cos = (1 + t^2)^(-1/2) by MUFU rsqrt + two Newton steps (branch-free).
+        const double d = be - al, g2 = 2.0 * ga;
+        const double h2 = fma(d, d, g2 * g2);
+        double rh = rsqrt_approx(h2);
+        rh = rh * fma(-0.5 * h2, rh * rh, 1.5);
+        const double den = fabs(d) + h2 * rh;
+        double rc = rcp_approx(den);
+        rc = rc * fma(-den, rc, 2.0);
+        const double t = (d >= 0.0 ? g2 : -g2) * rc;
+        const double y = fma(t, t, 1.0);
+        double cs = rsqrt_approx(y);
+        cs = cs * fma(-0.5 * y, cs * cs, 1.5);
+        cs = cs * fma(-0.5 * y, cs * cs, 1.5);
+        const double sn = cs * t;
 #pragma unroll
         for (int c = 0; c < EPL; ++c) {
           const int i = sub + G * c;
-          const bool ok = valid && i < n;
-          xp[c] = ok ? up[i] : 0.0;
-          xq[c] = ok ? uq[i] : 0.0;
-          if (c & 1) ga1 += xp[c] * xq[c]; else ga0 += xp[c] * xq[c];
+          if (i < n) { up[i] = cs * xp[c] - sn * xq[c]; uq[i] = sn * xp[c] + cs * xq[c]; }
         }
-        double ga = ga0 + ga1;
-#pragma unroll
-        for (int o = G / 2; o > 0; o >>= 1) ga += __shfl_xor_sync(0xffffffffu, ga, o);
-        const double al = valid ? nrm[p] : 1.0, be = valid ? nrm[q] : 1.0;
-        const double ab = al * be, g2a = ga * ga;
-        if (valid && ga != 0.0 && g2a > tol2 * ab) {
-          rotated = 1;
-          if (g2a > quad2 * ab) big = 1;
-          if (g2a > mid2 * ab) mid = 1;
-          // tan(theta) zeroing u_p.u_q: t = sign(d) g2 / (|d| + sqrt(d^2 + g2^2)),
-          // d = be - al, g2 = 2 ga. t needs only ~1e-10 relative accuracy (it just has to
-          // shrink u_p.u_q); (cs, sn) are exactly orthogonal to fp64 precision.
-          const double d = be - al, g2 = 2.0 * ga;
-          const double h2 = fma(d, d, g2 * g2);
-          double rh = rsqrt_approx(h2);
-          rh = rh * fma(-0.5 * h2, rh * rh, 1.5);
-          const double den = fabs(d) + h2 * rh;
-          double rc = rcp_approx(den);
-          rc = rc * fma(-den, rc, 2.0);
-          const double t = (d >= 0.0 ? g2 : -g2) * rc;
-          const double t2 = t * t;
-          double cs;
-          if (t2 < 1e-8) {          // cos = (1 + t^2)^(-1/2), series exact to 1e-24
-            cs = fma(t2, fma(t2, 0.375, -0.5), 1.0);
-          } else {
-            const double y = 1.0 + t2;
-            cs = rsqrt_approx(y);
-            cs = cs * fma(-0.5 * y, cs * cs, 1.5);
-            cs = cs * fma(-0.5 * y, cs * cs, 1.5);
-          }
-          const double sn = cs * t;
-#pragma unroll
-          for (int c = 0; c < EPL; ++c) {
-            const int i = sub + G * c;
-            if (i < n) { up[i] = cs * xp[c] - sn * xq[c]; uq[i] = sn * xp[c] + cs * xq[c]; }
-          }
-          if (sub == 0) {   // exact norms of the rotated pair from the 2x2 Gram matrix
-            const double c2 = cs * cs, s2 = sn * sn, csn = 2.0 * cs * sn * ga;
-            nrm[p] = c2 * al - csn + s2 * be;
-            nrm[q] = s2 * al + csn + c2 * be;
-          }
+        if (sub == 0) {   // exact norms of the rotated pair from the 2x2 Gram matrix
+          const double c2 = cs * cs, s2 = sn * sn, csn = 2.0 * cs * sn * ga;
+          nrm[p] = c2 * al - csn + s2 * be;
+          nrm[q] = s2 * al + csn + c2 * be;
         }
       }
-      __syncthreads();
+    };
+    if (nwarps * PPW >= H) {                   // every pair in one pass (warp-uniform)
+      const bool act = warp * PPW < H;
+      for (int r = 0; r < NP - 1; ++r) {
+        if (act) pair_step(r, warp * PPW + grp);
+        __syncthreads();
+      }
+    } else {
+      for (int r = 0; r < NP - 1; ++r) {
+        for (int P0 = warp * PPW; P0 < H; P0 += nwarps * PPW) pair_step(r, P0 + grp);
+        __syncthreads();
+      }
     }
     const int any_big = __syncthreads_or(big);
     const int any_rot = __syncthreads_or(rotated);

@@ -48,6 +48,14 @@ namespace {
 constexpr int kWarp = 32;
 constexpr int kGemvChunk = 8;       // vectors per warp in the dedup GEMV
 
+// Programmatic dependent launch: a kernel launched with programmatic stream
+// serialization may start while its predecessor runs; pdl_wait() blocks until the
+// predecessor grid has completed and its writes are visible (a no-op otherwise).
+// Every kernel triggers its dependents at entry.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_enter() { pdl_trigger(); pdl_wait(); }
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -141,6 +149,7 @@ __device__ __forceinline__ double cta_dot(const double *__restrict__ a, const do
 // ============================ K-TRSV phases ================================
 // P1: u_Q = r_Q - G r_L            (leaf elimination, forward)
 __global__ void k_solve_p1(SolveDev d, RhsArgs ra, const DevState *st) {
+  pdl_enter();
   if (st->done) return;
   const int qi = blockIdx.x * blockDim.x + threadIdx.x;
   if (qi >= d.nQ) return;
@@ -174,7 +183,7 @@ struct GemvItem { int32_t uid, row, list, cnt; };
 __global__ void __launch_bounds__(256) k_gemv_stage(SolveDev d, const GemvItem *items, int nitems,
                                                     int nsingle, const int32_t *stage_list, int mode,
                                                     const double *in, double *out, const DevState *st) {
-  if (st->done) return;
+  pdl_trigger();                  // item and factor addressing (static) before the wait
   __shared__ double sh[32];
   const int lane = threadIdx.x & 31;
   if ((int)blockIdx.x < nsingle) {
@@ -183,6 +192,8 @@ __global__ void __launch_bounds__(256) k_gemv_stage(SolveDev d, const GemvItem *
     const double *M = (mode == 0 ? d.Linv[it.uid] : d.LinvT[it.uid]) + (int64_t)it.row * n;
     const int jlo = mode == 0 ? 0 : it.row, jhi = mode == 0 ? it.row + 1 : n;
     const int b0 = d.R_off[stage_list[it.list]];
+    pdl_wait();
+    if (st->done) return;
     const double sum = cta_dot(M, in + b0, jlo, jhi, sh);
     if (threadIdx.x == 0) out[b0 + it.row] = sum;
     return;
@@ -200,6 +211,8 @@ __global__ void __launch_bounds__(256) k_gemv_stage(SolveDev d, const GemvItem *
     base[c] = c < it.cnt ? d.R_off[stage_list[it.list + c]] : 0;
     acc[c] = 0.0;
   }
+  pdl_wait();
+  if (st->done) return;
   int j = jlo + lane;
   for (; j + 32 < jhi; j += 64) {
     const double m0 = __ldg(M + j), m1 = __ldg(M + j + 32);
@@ -226,6 +239,7 @@ __global__ void __launch_bounds__(256) k_gemv_stage(SolveDev d, const GemvItem *
 // output and runs concurrently with P2). One warp per separator row (grid-stride over a
 // few CTAs per SM: the row dots are short, CTA dispatch was the cost), in place on u.
 __global__ void __launch_bounds__(256) k_solve_p3(SolveDev d, const DevState *st) {
+  pdl_enter();
   if (st->done) return;
   const int lane = threadIdx.x & 31;
   const int nw = (gridDim.x * blockDim.x) >> 5;
@@ -253,6 +267,7 @@ __global__ void __launch_bounds__(256) k_solve_p3(SolveDev d, const DevState *st
 constexpr int kSepTile = 64;
 __global__ void __launch_bounds__(256) k_sep_tri(SolveDev d, int mode, const double *in, double *out,
                                                  const DevState *st) {
+  pdl_enter();
   if (st->done) return;
   __shared__ double colp[8][kSepTile];
   __shared__ int last;
@@ -339,6 +354,7 @@ __global__ void k_pack_sep_tiles(int n, int nT, const double *C, double *tiles) 
 // P6'': y_Rk = w_Rk - H_k y_S,adj with w = L_k^{-T} L_k^{-1} u (P6'), H_k = L_k^{-T} F_k
 // (warp per interior row)
 __global__ void k_solve_p6a(SolveDev d, const int32_t *row_stage, double *y, const DevState *st) {
+  pdl_enter();
   if (st->done) return;
   const int lane = threadIdx.x & 31, nw = (gridDim.x * blockDim.x) >> 5;
   const int nR = d.S0 - d.nL;
@@ -360,6 +376,7 @@ __global__ void k_solve_p6a(SolveDev d, const int32_t *row_stage, double *y, con
 
 // P7: y_L = K_LL^{-1} r_L - G^T y_Q   (thread per leaf row)
 __global__ void k_solve_p7(SolveDev d, RhsArgs ra, double *y, const DevState *st) {
+  pdl_enter();
   if (st->done) return;
   const int l = blockIdx.x * blockDim.x + threadIdx.x;
   if (l >= d.nL) return;
@@ -408,6 +425,7 @@ __device__ void finalize_state(const double *part_ax, int nax, const double *par
 __global__ void k_spmv_ax(int m, const int64_t *rp, const int32_t *ci, const double *v, const double *x,
                           double *ax, const double *b, const double *y, double *part, const double *part_up,
                           int nup, DevState *st) {
+  pdl_enter();
   if (st->done) return;
   __shared__ double red[2 * 32];
   __shared__ int last;
@@ -438,6 +456,7 @@ __global__ void k_spmv_ax(int m, const int64_t *rp, const int32_t *ci, const dou
 __global__ void k_update(int64_t n, const int64_t *Atp, const int32_t *Atr, const double *Atv,
                          const double *y, double *X, const double *S, const double *C, const double *Xb,
                          double *part, const DevState *st) {
+  pdl_enter();
   if (st->done) return;
   __shared__ double red[4 * 32];
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -644,7 +663,38 @@ void mark(strom_admm *h, const char *name) {
   ++h->prof_idx;
 }
 
-strom_status launch_solve(strom_admm *h, const RhsArgs &ra, double *y, int &nl) {
+// Kernel launch with programmatic stream serialization (PDL) when `pdl`: the kernel may
+// begin (its static prologue) while the previous kernel on the stream is still running.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                     Args... args) {
+  if (!pdl) {
+    kern<<<grid, block, smem, s>>>(args...);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid; cfg.blockDim = block; cfg.dynamicSmemBytes = smem; cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at; cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
+// PDL on the main stream's kernel-to-kernel edges (not across fork/join events, not
+// while event nodes are captured for the per-kernel timing, not with the multi-rank
+// exchange). STROM_PDL is a bit mask over the edges (default kPdlDefault = none):
+// 1 P1, 2 P2, 4 P6', 8 P7, 16 K-EIG, 32 update, 64 A X. Measured at pendulum N=30
+// (216 us/iteration without): single edges move it by -5..+7 us, all edges +20 us (the
+// early-resident CTAs of the GEMVs slow their predecessors), so it stays off.
+enum { kPdlP1 = 1, kPdlP2 = 2, kPdlP6b = 4, kPdlP7 = 8, kPdlEig = 16, kPdlUpd = 32, kPdlAx = 64 };
+constexpr int kPdlDefault = 0;
+bool use_pdl(const strom_admm *h, int edge) {
+  static const int mask = [] { const char *e = getenv("STROM_PDL"); return e ? atoi(e) : kPdlDefault; }();
+  return (mask & edge) && !h->prof_capture && h->xfer == 0;
+}
+
+strom_status launch_solve(strom_admm *h, const RhsArgs &ra, double *y, int &nl, bool pdl_first = false) {
   // P1 -> { main: P2 (v = L^{-1} u), P6' (w = L^{-T} v) | fork: P3 (u_S -= H^T u_R), P4, P5 }
   //    -> join -> P6'' (y_R = w - H y_S) -> P7. Critical path 6 kernels.
   const SolveDev &d = h->sd;
@@ -652,7 +702,11 @@ strom_status launch_solve(strom_admm *h, const RhsArgs &ra, double *y, int &nl) 
   const int TB = 256;
   nl = 0;
   const int nR = d.S0 - d.nL;
-  if (d.nQ > 0) { mark(h, "trsv_p1_leaf_fwd"); k_solve_p1<<<(d.nQ + TB - 1) / TB, TB, 0, s>>>(d, ra, h->st); ++nl; }
+  if (d.nQ > 0) {
+    mark(h, "trsv_p1_leaf_fwd");
+    CK(launch_k(use_pdl(h, kPdlP1) && pdl_first, k_solve_p1, (d.nQ + TB - 1) / TB, TB, 0, s, d, ra, (const DevState *)h->st));
+    ++nl;
+  }
   const bool fork = d.nS > 0 && h->stream2;
   if (fork) {
     CK(cudaEventRecord(h->sfork_ev, s));
@@ -666,12 +720,13 @@ strom_status launch_solve(strom_admm *h, const RhsArgs &ra, double *y, int &nl) 
     k_sep_tri<<<ntl, 256, 0, s2>>>(d, 1, d.z + d.S0, y + d.S0, h->st); ++nl;
   }
   if (h->nitems > 0 && nR > 0) {
+    const int gg = h->nsingle + ((h->nitems - h->nsingle) * 32 + TB - 1) / TB;
     mark(h, "trsv_p2_stage_Linv");
-    k_gemv_stage<<<h->nsingle + ((h->nitems - h->nsingle) * 32 + TB - 1) / TB, TB, 0, s>>>(
-        d, h->items, h->nitems, h->nsingle, h->stage_list, 0, d.u, d.v, h->st);
+    CK(launch_k(use_pdl(h, kPdlP2) && d.nQ > 0, k_gemv_stage, gg, TB, 0, s, d, (const GemvItem *)h->items, h->nitems,
+                h->nsingle, (const int32_t *)h->stage_list, 0, (const double *)d.u, d.v, (const DevState *)h->st));
     mark(h, "trsv_p6b_stage_LinvT");
-    k_gemv_stage<<<h->nsingle + ((h->nitems - h->nsingle) * 32 + TB - 1) / TB, TB, 0, s>>>(
-        d, h->items, h->nitems, h->nsingle, h->stage_list, 1, d.v, d.nS > 0 ? d.t : y, h->st);
+    CK(launch_k(use_pdl(h, kPdlP6b), k_gemv_stage, gg, TB, 0, s, d, (const GemvItem *)h->items, h->nitems, h->nsingle,
+                (const int32_t *)h->stage_list, 1, (const double *)d.v, d.nS > 0 ? d.t : y, (const DevState *)h->st));
     nl += 2;
   }
   if (fork) {
@@ -682,7 +737,12 @@ strom_status launch_solve(strom_admm *h, const RhsArgs &ra, double *y, int &nl) 
     mark(h, "trsv_p6a_stage_H");
     k_solve_p6a<<<std::min((nR * 32 + TB - 1) / TB, 8 * h->num_sms), TB, 0, s>>>(d, h->row_stage_R, y, h->st); ++nl;
   }
-  if (d.nL > 0) { mark(h, "trsv_p7_leaf_bwd"); k_solve_p7<<<(d.nL + TB - 1) / TB, TB, 0, s>>>(d, ra, y, h->st); ++nl; }
+  if (d.nL > 0) {
+    mark(h, "trsv_p7_leaf_bwd");
+    const bool after_kernel = nR > 0 && d.nS > 0;   // P6'' on this stream just before
+    CK(launch_k(use_pdl(h, kPdlP7) && after_kernel, k_solve_p7, (d.nL + TB - 1) / TB, TB, 0, s, d, ra, y, (const DevState *)h->st));
+    ++nl;
+  }
   CK(cudaGetLastError());
   return STROM_OK;
 }
@@ -724,7 +784,8 @@ strom_status launch_eig(strom_admm *h, int mode, const double *yv, int &nl) {
       k_eig_cluster<<<a.nblk * kClusterEig, 512, eig_cluster_smem_bytes(h->eig_class_n[c]), s>>>(a);
     } else if (eig_global(np)) k_eig<32, 8, true><<<a.nblk, threads, smem, s>>>(a);
     else if (G == 4) k_eig<4, 4, false><<<a.nblk, threads, smem, s>>>(a);
-    else if (G == 8 && h->eig_class_n[c] <= 56) k_eig<8, 7, false><<<a.nblk, threads, smem, s>>>(a);
+    else if (G == 8 && h->eig_class_n[c] <= 56)
+      CK(launch_k(use_pdl(h, kPdlEig) && s == h->stream && mode == 0, k_eig<8, 7, false>, a.nblk, threads, smem, s, a));
     else if (G == 8) k_eig<8, 8, false><<<a.nblk, threads, smem, s>>>(a);
     else if (G == 32) k_eig<32, 2, false><<<a.nblk, threads, smem, s>>>(a);
     else k_eig<16, 8, false><<<a.nblk, threads, smem, s>>>(a);
@@ -744,7 +805,7 @@ strom_status launch_iteration_A(strom_admm *h, int &nl_total) {
   nl_total = 0;
   RhsArgs ra{h->b, h->AX, h->AC, h->Arp, h->Aci, h->Av, h->S, h->wrhs, nullptr};
   strom_status st;
-  if ((st = launch_solve(h, ra, h->yh, nl)) != STROM_OK) return st;       // Step 1
+  if ((st = launch_solve(h, ra, h->yh, nl, true)) != STROM_OK) return st;  // Step 1
   nl_total += nl;
   if ((st = launch_eig(h, 0, h->yh, nl)) != STROM_OK) return st;         // Step 2 (A* fused)
   nl_total += nl;
@@ -780,10 +841,13 @@ strom_status launch_iteration_B(strom_admm *h, int &nl_total) {
   nl_total += nl;
   // Step 4 + residual partials
   mark(h, "update_X");
-  k_update<<<h->nup, TB, 0, s>>>(h->n, h->Atp, h->Atr, h->Atv, h->y, h->X, h->S, h->C, h->Xb, h->part_up, h->st);
+  CK(launch_k(use_pdl(h, kPdlUpd), k_update, h->nup, TB, 0, s, h->n, (const int64_t *)h->Atp, (const int32_t *)h->Atr,
+              (const double *)h->Atv, (const double *)h->y, h->X, (const double *)h->S, (const double *)h->C,
+              (const double *)h->Xb, h->part_up, (const DevState *)h->st));
   mark(h, "spmv_AX_resid");
-  k_spmv_ax<<<h->nax, TB, 0, s>>>(h->m, h->Arp, h->Aci, h->Av, h->X, h->AX, h->b, h->y, h->part_ax,
-                                  h->part_up, h->nup, h->st);
+  CK(launch_k(use_pdl(h, kPdlAx), k_spmv_ax, h->nax, TB, 0, s, h->m, (const int64_t *)h->Arp, (const int32_t *)h->Aci,
+              (const double *)h->Av, (const double *)h->X, h->AX, (const double *)h->b, (const double *)h->y,
+              h->part_ax, (const double *)h->part_up, h->nup, h->st));
   mark(h, nullptr);
   nl_total += 2;
   CK(cudaGetLastError());
