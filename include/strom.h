@@ -169,6 +169,17 @@ strom_status strom_admm_get_device(strom_admm *h, double *dX, double *dy, double
 strom_status strom_admm_lower_bound(strom_admm *h, const double *R_beta, double *lb,
                                     double *lambda_min);
 
+/* Extraction data for the certificate ("extract a feasible solution
+ * from the eigenvectors of the moment matrices"), computed on the device at the current
+ * X by the K-EIG kernels in a cold eigendecomposition mode: for every block beta,
+ * lam12[2 beta] >= lam12[2 beta + 1] are the two largest eigenvalues of X_beta (their
+ * ratio is the tightness test: a rank-one moment matrix has lambda_2 = 0), and, when vtop
+ * is non-NULL, vtop[off_beta .. off_beta + n_beta) the unit eigenvector of the largest,
+ * sign fixed so that its first entry is >= 0 (off_beta = sum of n over earlier blocks;
+ * vtop holds sum_beta n_beta doubles). Host buffers owned by the caller; the iterate and
+ * the solver state are unchanged. EINVAL on NULL handle/lam12. */
+strom_status strom_admm_extract(strom_admm *h, double *lam12, double *vtop);
+
 /* Number of kernel launches one iteration issues (for launch accounting). */
 int32_t strom_admm_launches_per_iter(const strom_admm *h);
 /* Size of the factor data on the device in bytes, and unique dense factors. */

@@ -28,7 +28,7 @@ EXPORTS = [
     "strom_sdp_create", "strom_sdp_destroy", "strom_sdp_dims", "strom_admm_default_config",
     "strom_admm_setup", "strom_admm_destroy", "strom_admm_set_start",
     "strom_admm_set_start_device", "strom_admm_iterate", "strom_admm_solve", "strom_admm_get",
-    "strom_admm_get_device", "strom_admm_lower_bound", "strom_admm_launches_per_iter",
+    "strom_admm_get_device", "strom_admm_lower_bound", "strom_admm_extract", "strom_admm_launches_per_iter",
     "strom_admm_factor_info", "strom_admm_kernel_times", "strom_nccl_get_unique_id", "strom_last_error", "strom_version",
     "strom_debug_project_psd", "strom_debug_spmv", "strom_debug_solve", "strom_debug_host_solve",
     "strom_debug_eps", "strom_debug_link_virtual", "strom_debug_iterate_virtual",
@@ -91,6 +91,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "strom_admm_get": (I32, [VP, P(D), P(D), P(D), P(strom_residuals)]),
         "strom_admm_get_device": (I32, [VP, VP, VP, VP]),
         "strom_admm_lower_bound": (I32, [VP, P(D), P(D), P(D)]),
+        "strom_admm_extract": (I32, [VP, P(D), P(D)]),
         "strom_admm_launches_per_iter": (I32, [VP]),
         "strom_admm_factor_info": (I32, [VP, P(I64), P(I32), P(I32), P(I32)]),
         "strom_admm_kernel_times": (I32, [VP, P(D), P(C.c_char_p), I32]),
@@ -179,6 +180,7 @@ class StromSdp:
         self.m = m
         self.n = int(bo[-1])
         self.nblocks = len(bn)
+        self.block_n = bn.copy()
 
     def dims(self):
         n, m, nb = C.c_int64(), C.c_int32(), C.c_int32()
@@ -275,6 +277,17 @@ class StromAdmm:
         _check(load().strom_admm_lower_bound(self.handle, _dptr(R), C.byref(lb), _dptr(lam)),
                "strom_admm_lower_bound")
         return lb.value, lam
+
+    def extract(self):
+        """(lam12 [nblocks, 2], [top unit eigenvector of each block]) of the current X,
+        computed on the device (strom_admm_extract)."""
+        nb = self.sdp.nblocks
+        bn = np.asarray(self.sdp.block_n, dtype=np.int64)
+        lam12 = np.zeros(2 * nb)
+        vtop = np.zeros(int(bn.sum()))
+        _check(load().strom_admm_extract(self.handle, _dptr(lam12), _dptr(vtop)), "strom_admm_extract")
+        offs = np.concatenate([[0], np.cumsum(bn)])
+        return lam12.reshape(nb, 2), [vtop[offs[k]:offs[k + 1]] for k in range(nb)]
 
     def kernel_times(self):
         """[(kernel name, ms)] of the instrumented iteration of the last graph launch."""

@@ -31,8 +31,10 @@ def _block_matrix(svec: np.ndarray, n: int) -> np.ndarray:
     return M
 
 
-def extract_zbar(sdp, X: np.ndarray) -> np.ndarray:
-    """Steps one and two of the extraction heuristic."""
+def extract_zbar(sdp, X: np.ndarray, vtop=None) -> np.ndarray:
+    """Steps one and two of the extraction heuristic. `vtop`: the top
+    eigenvectors computed on the GPU (StromAdmm.extract(), strom_admm_extract); else
+    LAPACK on the host."""
     pop = sdp.meta["pop"]
     bo = np.asarray(sdp.block_offset)
     acc = np.zeros(pop.d)
@@ -40,8 +42,11 @@ def extract_zbar(sdp, X: np.ndarray) -> np.ndarray:
     for k, I in enumerate(pop.cliques):
         beta = sdp.meta["mom_block"][k]
         nb = int(sdp.block_n[beta])
-        w, Q = np.linalg.eigh(_block_matrix(X[bo[beta]:bo[beta + 1]], nb))
-        v = Q[:, -1] / Q[0, -1]
+        if vtop is not None:
+            q = np.asarray(vtop[beta])
+        else:
+            q = np.linalg.eigh(_block_matrix(X[bo[beta]:bo[beta + 1]], nb))[1][:, -1]
+        v = q / q[0]
         for j, e in enumerate(sdp.meta["basis"][k]):
             if sum(e) == 1:
                 var = int(np.argmax(e))
@@ -50,7 +55,7 @@ def extract_zbar(sdp, X: np.ndarray) -> np.ndarray:
     return acc / np.maximum(cnt, 1)
 
 
-def pendulum_upper_bound(sdp, X: np.ndarray, maxiter: int = 200, u_start=None):
+def pendulum_upper_bound(sdp, X: np.ndarray, maxiter: int = 200, u_start=None, vtop=None):
     """p_hat for the pendulum POP: controls of z_bar, then a local solve over the
     controls (rollouts satisfy x_0 = x_init, the dynamics and SO(2) exactly;
     |u| <= 1 and fc_k >= fc_min are the local solver's constraints)."""
@@ -61,7 +66,7 @@ def pendulum_upper_bound(sdp, X: np.ndarray, maxiter: int = 200, u_start=None):
     N = pop.N
     p = pop.meta["params"]
     th0, thd0 = pop.meta["theta0"], pop.meta["theta_dot0"]
-    zbar = extract_zbar(sdp, X)
+    zbar = extract_zbar(sdp, X, vtop)
     u0 = np.clip(np.array([zbar[5 * k + 4] for k in range(N)]), -1.0, 1.0)
     if u_start is not None:   # keep the better of the extracted and the previous controls
         if pop.objective(pendulum_rollout(N, u_start, th0, thd0, p)) < pop.objective(pendulum_rollout(N, u0, th0, thd0, p)):

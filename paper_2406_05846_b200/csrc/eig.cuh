@@ -32,7 +32,9 @@ struct EigArgs {
   double *Ug, *Ag; const int64_t *uoff;    // global scratch for n > 112 (GU variant)
   DevState *st;
   int32_t max_sweeps; double tol;
-  int32_t mode;          // 0 projection; 1 eigenvalues of C - A*y (lambda_min only)
+  int32_t mode;          // 0 projection; 1 eigenvalues of C - A*y (lambda_min only);
+                         // 2 extraction: top two eigenvalues and top eigenvector of X
+  double *lam12; double *vtop; const int64_t *toff;   // mode 2 outputs (toff: prefix of n)
   int32_t warm_enable, cold_every;
   double *lam_min;
 };
@@ -126,7 +128,7 @@ __device__ __forceinline__ double gather_xb(const EigArgs &a, int64_t off, int L
       const int e = eb + k * es;
       if (e < L) {
         const int64_t J = off + e;
-        const double xb = proj ? a.X[J] + sigma * (aty[k] - a.C[J]) : a.C[J] - aty[k];
+        const double xb = a.mode == 2 ? a.X[J] : proj ? a.X[J] + sigma * (aty[k] - a.C[J]) : a.C[J] - aty[k];
         a.Xb_out[J] = xb;          // mode 1 uses Xb_out as scratch for C - A*y
         fro += xb * xb;            // svec norm == Frobenius norm
       }
@@ -184,7 +186,7 @@ __device__ __forceinline__ double gather_xb_smem(const EigArgs &a, int64_t off, 
     if (e < L) {
       const int64_t J = off + e;
       t0[k] = (int)(a.Atp[J] - nz0); t1[k] = (int)(a.Atp[J + 1] - nz0);
-      if (proj) xk[k] = a.X[J];
+      if (proj || a.mode == 2) xk[k] = a.X[J];
       ck[k] = a.C[J];
     }
   }
@@ -196,7 +198,7 @@ __device__ __forceinline__ double gather_xb_smem(const EigArgs &a, int64_t off, 
     if (e < L) {
       double aty = 0.0;
       for (int t = t0[k]; t < t1[k]; ++t) aty += prod[t];
-      const double xb = proj ? xk[k] + sigma * (aty - ck[k]) : ck[k] - aty;
+      const double xb = a.mode == 2 ? xk[k] : proj ? xk[k] + sigma * (aty - ck[k]) : ck[k] - aty;
       a.Xb_out[off + e] = xb;
       fro += xb * xb;
       xv[k] = xb;
@@ -255,6 +257,21 @@ __device__ __forceinline__ void warm_product_tiles(const double *Abuf, const dou
         if (i < n && j < n) dst[(int64_t)j * ld + i] = acc[r][c] + s * vij[r][c];
       }
   }
+}
+
+// Extraction outputs (mode 2): the two largest eigenvalues of the block
+// and the eigenvector of the largest, normalised, sign fixed so that its first entry is
+// >= 0. Rows [r0, r0 + nloc) of column j are at col[i - r0]; inv = 1/||u_j||, and v0 =
+// the column's first entry (row 0, any CTA).
+__device__ __forceinline__ int top2(const double *lam, int n, double &l1, double &l2) {
+  int j = 0;
+  l1 = lam[0]; l2 = -1.0e308;
+  for (int k = 1; k < n; ++k) {
+    if (lam[k] > l1) { l2 = l1; l1 = lam[k]; j = k; }
+    else if (lam[k] > l2) l2 = lam[k];
+  }
+  if (n == 1) l2 = 0.0;
+  return j;
 }
 
 // Convergence check by the Gram matrix U^T U (4x4 register tiles, upper triangle):
@@ -600,6 +617,15 @@ __global__ void __launch_bounds__(512, 1) k_eig(EigArgs a) {
   V = U;                          // eigenvectors now live in the U buffer
   __syncthreads();
   const double *lam = lamv;
+  if (a.mode == 2) {
+    double l1, l2;
+    const int j = top2(lam, n, l1, l2);
+    if (tid == 0) { a.lam12[2 * bidx] = l1; a.lam12[2 * bidx + 1] = l2; }
+    const double inv = GU ? 1.0 : wsc[128 + j];
+    const double sg = V[j * ld] < 0.0 ? -inv : inv;
+    for (int i = tid; i < n; i += nt) a.vtop[a.toff[bidx] + i] = V[j * ld + i] * sg;
+    return;
+  }
   if (!proj) {
     if (tid == 0) {
       double lm = lam[0];
@@ -940,6 +966,16 @@ __global__ void __cluster_dims__(kClusterEig, 1, 1) __launch_bounds__(512, 1) k_
   for (int j = tid; j < n; j += nt) lamv[j] = nrm[j] - s;
   __syncthreads();
   const double *lam = lamv;
+  if (a.mode == 2) {
+    double l1, l2;
+    const int j = top2(lam, n, l1, l2);
+    if (tid == 0 && crank == 0) { a.lam12[2 * bidx] = l1; a.lam12[2 * bidx + 1] = l2; }
+    const double v0 = cl.map_shared_rank(U, 0)[j * h];     // row 0 lives in CTA 0
+    const double sg = v0 < 0.0 ? -1.0 / nrm[j] : 1.0 / nrm[j];
+    for (int il = tid; il < nloc; il += nt) a.vtop[a.toff[bidx] + r0 + il] = U[j * h + il] * sg;
+    cl.sync();                                      // CTA 0's shared memory read by CTA 1
+    return;
+  }
   if (!proj) {
     if (tid == 0 && crank == 0) {
       double lm = lam[0];

@@ -582,6 +582,7 @@ struct strom_admm {
   int launches_per_iter = 0;
   int num_sms = 148;
   double *lam_dev = nullptr;
+  double *lam12_dev = nullptr, *vtop_dev = nullptr; int64_t *toff_dev = nullptr;   // extraction
   double *Vstore = nullptr; int64_t *voff = nullptr;
   double *Ug = nullptr, *Ag = nullptr; int64_t *uoff = nullptr;
   // per-kernel event instrumentation of one iteration inside the K-graph
@@ -762,7 +763,7 @@ strom_status launch_eig(strom_admm *h, int mode, const double *yv, int &nl) {
   for (int c = 0; c < ncls; ++c) {
     const int np = h->eig_class_np[c];
     EigArgs a;
-    const bool all = (mode == 1);               // the lower bound needs every block
+    const bool all = (mode != 0);               // the lower bound / extraction need every block
     a.blocks = all ? h->eig_class_dev_all[c] : h->eig_class_dev[c];
     a.nblk = (int)(all ? h->eig_class_all[c].size() : h->eig_class_blocks[c].size());
     if (a.nblk == 0) continue;
@@ -772,6 +773,7 @@ strom_status launch_eig(strom_admm *h, int mode, const double *yv, int &nl) {
     a.Xb_out = h->Xb; a.S_out = h->S; a.st = h->st;
     a.max_sweeps = h->cfg.eig_max_sweeps; a.tol = h->cfg.eig_tol;
     a.mode = mode; a.lam_min = h->lam_dev;
+    a.lam12 = h->lam12_dev; a.vtop = h->vtop_dev; a.toff = h->toff_dev;
     a.Vstore = h->Vstore; a.voff = h->voff;
     a.warm_enable = h->cfg.eig_warm; a.cold_every = h->cfg.eig_cold_every;
     const int threads = eig_threads(np);
@@ -1216,7 +1218,8 @@ strom_status strom_admm_setup(strom_admm **out, const strom_sdp *sdp_h, const st
       (st = h->alloc(h->y, m)) || (st = h->alloc(h->yh, m)) || (st = h->alloc(h->AX, m)) ||
       (st = h->alloc(h->AC, m)) || (st = h->alloc(h->zeros_m, m)) || (st = h->alloc(h->wrhs, m)) ||
       (st = h->alloc(h->tmp_m, std::max<int64_t>(m, s.n))) || (st = h->alloc(h->tmp_m2, std::max<int64_t>(m, s.n))) ||
-      (st = h->alloc(h->st, 1)) || (st = h->alloc(h->lam_dev, s.nblocks)))
+      (st = h->alloc(h->st, 1)) || (st = h->alloc(h->lam_dev, s.nblocks)) ||
+      (st = h->alloc(h->lam12_dev, 2 * (size_t)s.nblocks)))
     return st;
   CK(cudaMemset(h->X, 0, sizeof(double) * s.n));
   CK(cudaMemset(h->S, 0, sizeof(double) * s.n));
@@ -1499,6 +1502,36 @@ strom_status strom_admm_get_device(strom_admm *h, double *dX, double *dy, double
   if (dS) CK(cudaMemcpyAsync(dS, h->S, sizeof(double) * h->n, cudaMemcpyDeviceToDevice, h->stream));
   if (dy) k_permute<<<(h->m + 255) / 256, 256, 0, h->stream>>>(h->m, h->perm, h->y, dy, 1);
   CK(cudaGetLastError());
+  return STROM_OK;
+}
+
+strom_status strom_admm_extract(strom_admm *h, double *lam12, double *vtop) {
+  if (!h || !lam12) { set_error("strom_admm_extract: NULL argument"); return STROM_EINVAL; }
+  CK(cudaSetDevice(h->device));
+  const int nb = h->nblocks;
+  std::vector<int32_t> bn(nb);
+  CK(d2h(h, bn.data(), h->bn, sizeof(int32_t) * nb));
+  int64_t nt = 0;
+  for (int k = 0; k < nb; ++k) nt += bn[k];
+  if (!h->vtop_dev) {            // first call: per-block offsets of the top eigenvectors
+    std::vector<int64_t> toff(nb + 1, 0);
+    for (int k = 0; k < nb; ++k) toff[k + 1] = toff[k] + bn[k];
+    strom_status st = h->upload(h->toff_dev, toff);
+    if (st == STROM_OK) st = h->alloc(h->vtop_dev, (size_t)nt);
+    if (st) return st;
+  }
+  DevState ds;
+  CK(d2h(h, &ds, h->st, sizeof(DevState)));
+  const int32_t done_old = ds.done;
+  const int32_t zero = 0;
+  CK(cudaMemcpyAsync(&h->st->done, &zero, sizeof(int32_t), cudaMemcpyHostToDevice, h->stream));
+  int nl = 0;
+  strom_status st = launch_eig(h, 2, h->y, nl);
+  if (st) return st;
+  CK(cudaMemcpyAsync(&h->st->done, &done_old, sizeof(int32_t), cudaMemcpyHostToDevice, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  CK(d2h(h, lam12, h->lam12_dev, sizeof(double) * 2 * nb));
+  if (vtop) CK(d2h(h, vtop, h->vtop_dev, sizeof(double) * nt));
   return STROM_OK;
 }
 

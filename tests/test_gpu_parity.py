@@ -294,3 +294,44 @@ def test_graft_smoke_entry():
     """The driver's smoke() (pendulum N=3, 5 iterations vs the oracle) runs as shipped."""
     import __graft_entry__
     __graft_entry__.smoke()
+
+
+@pytest.mark.parametrize("name", ["pend5", "wide190"])
+def test_extract_parity(name):
+    """strom_admm_extract (certificate extraction) against LAPACK on the
+    same X: the two largest eigenvalues of every block and the top eigenvector (unit,
+    first entry >= 0), for shared-memory (55/10) and cluster (190) K-EIG variants."""
+    sdp = case(name)
+    g = make(sdp)
+    g.iterate(30)
+    X, _, _, _ = g.get()
+    lam12, vtop = g.extract()
+    bo = np.asarray(sdp.block_offset)
+    for beta, nb in enumerate(np.asarray(sdp.block_n)):
+        M = svec_to_mat(X[bo[beta]:bo[beta + 1]], int(nb))
+        w, Q = np.linalg.eigh(M)
+        scale = max(1.0, np.abs(w).max())
+        assert abs(lam12[beta, 0] - w[-1]) <= 1e-11 * scale
+        if nb > 1:
+            assert abs(lam12[beta, 1] - w[-2]) <= 1e-11 * scale
+        if nb > 1 and w[-1] - w[-2] > 1e-6 * scale:     # top eigenvector is unique
+            q = Q[:, -1] * (1.0 if Q[0, -1] >= 0 else -1.0)
+            assert np.linalg.norm(vtop[beta] - q) <= 1e-8
+        assert abs(np.linalg.norm(vtop[beta]) - 1.0) <= 1e-12
+    # the iterate and the state are unchanged by the extraction
+    X2, _, _, r2 = g.get()
+    assert np.array_equal(X, X2)
+
+
+def test_certificate_with_gpu_extraction():
+    """The certificate's extraction step from the GPU top eigenvectors gives the same
+    z_bar as LAPACK on the host."""
+    from paper_2406_05846_b200 import certify
+    sdp = case("pend5")
+    g = make(sdp)
+    g.iterate(400)
+    X, _, _, _ = g.get()
+    _, vtop = g.extract()
+    z_gpu = certify.extract_zbar(sdp, X, vtop)
+    z_host = certify.extract_zbar(sdp, X)
+    assert np.allclose(z_gpu, z_host, rtol=1e-7, atol=1e-9)
