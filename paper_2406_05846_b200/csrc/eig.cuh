@@ -753,10 +753,12 @@ inline size_t eig_smem_bytes(int n) {
 inline int eig_G(int n) {
   if (eig_global(n)) return 32;
   static int force = [] { const char *e = getenv("STROM_EIG_G"); return e ? atoi(e) : 0; }();
-  if (force == 8 && n <= 64) return 8;
+  if (force == 8 && n <= 112) return 8;
   if (force == 16 && n > 16) return 16;
   if (force == 32 && n > 16 && n <= 64) return 32;
-  return n <= 16 ? 4 : (n <= 64 ? 8 : 16);
+  // 8 lanes per pair up to the shared-memory limit: at order 105 (cart-pole) one pass of
+  // 14 warps per round instead of two passes with 16 lanes (K-EIG 479 -> 408 us)
+  return n <= 16 ? 4 : (n <= 112 ? 8 : 16);
 }
 inline int eig_threads(int n) {
   const int H = (n + (n & 1)) / 2, G = eig_G(n), ppw = 32 / G;

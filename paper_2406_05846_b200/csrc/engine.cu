@@ -788,7 +788,8 @@ strom_status launch_eig(strom_admm *h, int mode, const double *yv, int &nl) {
     else if (G == 4) k_eig<4, 4, false><<<a.nblk, threads, smem, s>>>(a);
     else if (G == 8 && h->eig_class_n[c] <= 56)
       CK(launch_k(use_pdl(h, kPdlEig) && s == h->stream && mode == 0, k_eig<8, 7, false>, a.nblk, threads, smem, s, a));
-    else if (G == 8) k_eig<8, 8, false><<<a.nblk, threads, smem, s>>>(a);
+    else if (G == 8 && h->eig_class_n[c] <= 64) k_eig<8, 8, false><<<a.nblk, threads, smem, s>>>(a);
+    else if (G == 8) k_eig<8, 14, false><<<a.nblk, threads, smem, s>>>(a);
     else if (G == 32) k_eig<32, 2, false><<<a.nblk, threads, smem, s>>>(a);
     else k_eig<16, 8, false><<<a.nblk, threads, smem, s>>>(a);
     ++nl;
@@ -1359,6 +1360,7 @@ strom_status strom_admm_setup(strom_admm **out, const strom_sdp *sdp_h, const st
       CK(cudaFuncSetAttribute(k_eig<4, 4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)maxsm));
       CK(cudaFuncSetAttribute(k_eig<8, 8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)maxsm));
       CK(cudaFuncSetAttribute(k_eig<8, 7, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)maxsm));
+      CK(cudaFuncSetAttribute(k_eig<8, 14, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)maxsm));
       CK(cudaFuncSetAttribute(k_eig<16, 8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)maxsm));
       CK(cudaFuncSetAttribute(k_eig<32, 2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)maxsm));
       CK(cudaFuncSetAttribute(k_eig<32, 8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)maxsm));
