@@ -789,6 +789,8 @@ inline size_t eig_cluster_smem_bytes(int n) {
   return sizeof(double) * ((size_t)h * n + n /*norms*/ + n /*lambda*/ + 2 * (size_t)H /*partials*/ + 16);
 }
 
+// G lanes per column pair, EPL >= h/G local rows per lane.
+template <int G, int EPL>
 __global__ void __cluster_dims__(kClusterEig, 1, 1) __launch_bounds__(512, 1) k_eig_cluster(EigArgs a) {
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
@@ -797,7 +799,7 @@ __global__ void __cluster_dims__(kClusterEig, 1, 1) __launch_bounds__(512, 1) k_
   __shared__ double red[4 * 32];
   __shared__ int sets[128];
   __shared__ int set_info;
-  constexpr int G = 16, EPL = 8, PPW = 32 / G;   // h <= 118 rows per CTA -> 8 rows per lane
+  constexpr int PPW = 32 / G;
   const int crank = (int)cl.block_rank();
   const int bidx = a.blocks[blockIdx.x / kClusterEig];
   const int n = a.bn[bidx];

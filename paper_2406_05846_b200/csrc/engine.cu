@@ -783,7 +783,11 @@ strom_status launch_eig(strom_admm *h, int mode, const double *yv, int &nl) {
     a.Ug = h->Ug; a.Ag = h->Ag; a.uoff = h->uoff;
     const int G = eig_G(np);
     if (eig_use_cluster(h->eig_class_n[c])) {
-      k_eig_cluster<<<a.nblk * kClusterEig, 512, eig_cluster_smem_bytes(h->eig_class_n[c]), s>>>(a);
+      // 16 lanes per pair (three passes per round phase at order 190). 8 lanes (two passes,
+      // 15 rows per lane; STROM_EIG_CL8=1) measured slower: car back-in K-EIG 4.02 -> 4.59 ms.
+      static const bool cl8 = [] { const char *e = getenv("STROM_EIG_CL8"); return e && e[0] == '1'; }();
+      if (cl8) k_eig_cluster<8, 15><<<a.nblk * kClusterEig, 512, eig_cluster_smem_bytes(h->eig_class_n[c]), s>>>(a);
+      else k_eig_cluster<16, 8><<<a.nblk * kClusterEig, 512, eig_cluster_smem_bytes(h->eig_class_n[c]), s>>>(a);
     } else if (eig_global(np)) k_eig<32, 8, true><<<a.nblk, threads, smem, s>>>(a);
     else if (G == 4) k_eig<4, 4, false><<<a.nblk, threads, smem, s>>>(a);
     else if (G == 8 && h->eig_class_n[c] <= 56)
@@ -1325,8 +1329,12 @@ strom_status strom_admm_setup(strom_admm **out, const strom_sdp *sdp_h, const st
       for (int k : h->eig_class_blocks[c]) mx = std::max(mx, s.bn[k]);
       h->eig_class_n.push_back(mx);
       if (eig_use_cluster(mx))
-        CK(cudaFuncSetAttribute(k_eig_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      {
+        CK(cudaFuncSetAttribute(k_eig_cluster<16, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)eig_cluster_smem_bytes(mx)));
+        CK(cudaFuncSetAttribute(k_eig_cluster<8, 15>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)eig_cluster_smem_bytes(mx)));
+      }
     }
     double best = -1.0;
     for (size_t c = 0; c < nps.size(); ++c) {
