@@ -1444,14 +1444,23 @@ static strom_status set_tol(strom_admm *h, double tol) {
   return STROM_OK;
 }
 
+}  // extern "C"
+namespace {
+// tol := tol, done := 0 as a stream-ordered kernel: a pageable host->device copy would
+// synchronise the stream first and serialise the handles of a batch on one host thread
+__global__ void k_set_control(DevState *st, double tol) {
+  st->tol = tol;
+  st->done = 0;
+}
+}  // namespace
+extern "C" {
+
 strom_status strom_admm_iterate(strom_admm *h, int64_t iters) {
   if (!h || iters < 0) { set_error("strom_admm_iterate: bad arguments"); return STROM_EINVAL; }
   CK(cudaSetDevice(h->device));
-  // iterate() never stops early: clear done and disable tol
-  const int32_t zero = 0;
-  strom_status st = set_tol(h, -1.0);
-  if (st) return st;
-  CK(cudaMemcpyAsync(&h->st->done, &zero, sizeof(int32_t), cudaMemcpyHostToDevice, h->stream));
+  // iterate() never stops early: clear done and disable tol (fully asynchronous)
+  k_set_control<<<1, 1, 0, h->stream>>>(h->st, -1.0);
+  CK(cudaGetLastError());
   int64_t left = iters;
   while (left >= h->K) { CK(cudaGraphLaunch(h->execK, h->stream)); left -= h->K; }
   while (left > 0) { CK(cudaGraphLaunch(h->exec1, h->stream)); --left; }
