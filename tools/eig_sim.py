@@ -35,7 +35,7 @@ def schedule(n):
     return rounds
 
 
-def jacobi(A, V0, cross_only=False, max_sweeps=40, mid_thr=1e-12):
+def jacobi(A, V0, cross_only=False, max_sweeps=40, mid_thr=1e-12, big_thr=1e-18):
     n = A.shape[0]
     s = 2.0 * np.linalg.norm(A)
     U = (A + s * np.eye(n)) @ V0
@@ -44,6 +44,7 @@ def jacobi(A, V0, cross_only=False, max_sweeps=40, mid_thr=1e-12):
     for sweep in range(max_sweeps):
         nrm = (U * U).sum(0)
         big = mid = rot = False
+        big_corr = False
         for pr in sched:
             p, q = pr[:, 0], pr[:, 1]
             up, uq = U[:, p], U[:, q]
@@ -57,7 +58,8 @@ def jacobi(A, V0, cross_only=False, max_sweeps=40, mid_thr=1e-12):
             if not sel.any():
                 continue
             rot = True
-            big |= bool((ga[sel] ** 2 > 1e-18 * ab[sel]).any())
+            big |= bool((ga[sel] ** 2 > big_thr * ab[sel]).any())
+            big_corr |= bool((ga[sel] ** 2 > 1e-10 * ab[sel]).any())
             mid |= bool((ga[sel] ** 2 > mid_thr * ab[sel]).any())
             d = be - al
             g2 = 2 * ga
@@ -73,6 +75,22 @@ def jacobi(A, V0, cross_only=False, max_sweeps=40, mid_thr=1e-12):
             nrm[q] = (nuq * nuq).sum(0)
         if not rot or not big:
             return sweep + 1, U, s
+        if CORR and not big_corr:
+            # first-order simultaneous correction U <- U (I + Theta) from the Gram matrix
+            G = U.T @ U
+            nn = np.diag(G).copy()
+            dn = np.sqrt(np.outer(nn, nn))
+            cosm = np.abs(G) / dn
+            np.fill_diagonal(cosm, 0.0)
+            D = nn[None, :] - nn[:, None]          # D[p, q] = n_q - n_p
+            with np.errstate(divide="ignore", invalid="ignore"):
+                Th = np.where(cosm > 1e-12, G / D, 0.0)
+            np.fill_diagonal(Th, 0.0)
+            Th = np.triu(Th, 1)
+            if np.all(np.isfinite(Th)) and np.abs(Th).max() <= 1e-6:
+                Th = Th - Th.T
+                U = U + U @ Th
+                return sweep + 1.3, U, s
         if not mid:
             G = U.T @ U
             dn = np.sqrt(np.outer(np.diag(G), np.diag(G)))
@@ -97,6 +115,8 @@ def proj_from(U, s, A, cross_only):
 
 
 MID = float(os.environ.get('MID', '1e-8'))
+BIG = float(os.environ.get('BIG', '1e-18'))
+CORR = os.environ.get('CORR', '0') == '1'
 
 
 def main():
@@ -130,14 +150,14 @@ def main():
             V0 = Vw.get(i, np.eye(bn[i]))
             P_ref = (lambda W, Q: (Q * np.maximum(W, 0)) @ Q.T)(*np.linalg.eigh(A))
             for co, thr in ((False, 1e-12), (True, MID)):
-                ns, U, s = jacobi(A, V0.copy(), False, mid_thr=thr)
+                ns, U, s = jacobi(A, V0.copy(), False, mid_thr=thr, big_thr=(BIG if co else 1e-18))
                 P, _ = proj_from(U, s, A, False)
                 sw[co].append(ns)
                 if co:
                     err = max(err, np.abs(P - P_ref).max() / max(1.0, np.abs(A).max()))
             Vw[i] = np.linalg.eigh(A)[1]
         print(f"iter {k:4d}: full sweeps mean {np.mean(sw[False]):.2f} max {max(sw[False])} | "
-              f"mid={MID:g} mean {np.mean(sw[True]):.2f} max {max(sw[True])}  proj err {err:.1e}")
+              f"mid={MID:g} big={BIG:g} mean {np.mean(sw[True]):.2f} max {max(sw[True])}  proj err {err:.1e}")
 
 
 if __name__ == "__main__":
