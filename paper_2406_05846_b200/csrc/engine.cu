@@ -684,12 +684,12 @@ cudaError_t launch_k(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, si
 
 // PDL on the main stream's kernel-to-kernel edges (not across fork/join events, not
 // while event nodes are captured for the per-kernel timing, not with the multi-rank
-// exchange). STROM_PDL is a bit mask over the edges (default kPdlDefault = none):
-// 1 P1, 2 P2, 4 P6', 8 P7, 16 K-EIG, 32 update, 64 A X. Measured at pendulum N=30
-// (216 us/iteration without): single edges move it by -5..+7 us, all edges +20 us (the
-// early-resident CTAs of the GEMVs slow their predecessors), so it stays off.
+// exchange). STROM_PDL is a bit mask over the edges (default kPdlDefault):
+// 1 P1, 2 P2, 4 P6', 8 P7, 16 K-EIG, 32 update, 64 A X. Measured at pendulum N=30: all
+// edges +20 us (the early-resident CTAs of the GEMVs slow their predecessors); K-EIG
+// (its schedule table is built while P7 drains) and A X: 211 -> 207 us, repeatable.
 enum { kPdlP1 = 1, kPdlP2 = 2, kPdlP6b = 4, kPdlP7 = 8, kPdlEig = 16, kPdlUpd = 32, kPdlAx = 64 };
-constexpr int kPdlDefault = 0;
+constexpr int kPdlDefault = kPdlEig | kPdlAx;
 bool use_pdl(const strom_admm *h, int edge) {
   static const int mask = [] { const char *e = getenv("STROM_PDL"); return e ? atoi(e) : kPdlDefault; }();
   return (mask & edge) && !h->prof_capture && h->xfer == 0;
