@@ -75,6 +75,13 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         return _lib
     if not os.path.exists(path):
         raise ImportError(f"libstrom.so not built at {path}; run paper_2406_05846_b200/build.py")
+    # torch first: libstrom resolves libnccl.so.2 to the NCCL torch already loaded (the
+    # system libnccl loaded first would leave torch's CUDA library with unresolved
+    # NCCL symbols when torch is imported afterwards)
+    try:
+        import torch  # noqa: F401
+    except ImportError:
+        pass
     lib = C.CDLL(path)
     P, VP, D, I32, I64 = C.POINTER, C.c_void_p, C.c_double, C.c_int32, C.c_int64
     sig = {

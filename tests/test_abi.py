@@ -123,3 +123,14 @@ def test_setup_rejects_bad_config(lib):
         with pytest.raises(S.StromError) as e:
             S.StromAdmm(h, cfg)
         assert e.value.status == -1
+
+
+def test_handle_calls_validate_arguments(lib):
+    """Entry points on a NULL handle return STROM_EINVAL (no GPU needed)."""
+    import ctypes as C
+    lam12 = (C.c_double * 4)()
+    assert lib.strom_admm_extract(None, lam12, None) == -1
+    assert lib.strom_admm_extract(None, None, None) == -1
+    lb = C.c_double()
+    assert lib.strom_admm_lower_bound(None, lam12, C.byref(lb), None) == -1
+    assert lib.strom_admm_iterate(None, 1) == -1

@@ -117,6 +117,7 @@ def proj_from(U, s, A, cross_only):
 MID = float(os.environ.get('MID', '1e-8'))
 BIG = float(os.environ.get('BIG', '1e-18'))
 CORR = os.environ.get('CORR', '0') == '1'
+EVERY = os.environ.get('EVERY', '0') == '1'
 
 
 def main():
@@ -137,7 +138,7 @@ def main():
     big = [i for i in range(len(bn)) if bn[i] == bn.max()]
     Vw = {}
     for k in range(len(rec)):
-        if k % 25 and k < len(rec) - 5 and k > 5:
+        if (k % 25 and k < len(rec) - 5 and k > 5) and not (EVERY and k >= len(rec) - 50):
             # keep the warm basis current without recording
             for i in big:
                 A = svec_to_mat(rec[k][bo[i]:bo[i + 1]], bn[i])
