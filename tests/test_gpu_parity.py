@@ -335,3 +335,25 @@ def test_certificate_with_gpu_extraction():
     z_gpu = certify.extract_zbar(sdp, X, vtop)
     z_host = certify.extract_zbar(sdp, X)
     assert np.allclose(z_gpu, z_host, rtol=1e-7, atol=1e-9)
+
+
+def test_concurrent_handles_match_sequential():
+    """Two handles on their own streams iterated back to back (strom_admm_iterate is
+    asynchronous) give bitwise the iterates of separate sequential runs."""
+    sdp_a, sdp_b = case("pend5"), case("pend3")
+    runs = []
+    for concurrent in (False, True):
+        ga, gb = make(sdp_a), make(sdp_b)
+        if concurrent:
+            for _ in range(4):
+                ga.iterate(10)
+                gb.iterate(10)
+        else:
+            ga.iterate(40)
+            gb.iterate(40)
+        runs.append((ga.get(), gb.get()))
+    (a0, b0), (a1, b1) = runs
+    for u, v in ((a0, a1), (b0, b1)):
+        for k in range(3):
+            assert np.array_equal(u[k], v[k])
+        assert u[3]["iter"] == v[3]["iter"] == 40
