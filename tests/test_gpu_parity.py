@@ -357,3 +357,31 @@ def test_concurrent_handles_match_sequential():
         for k in range(3):
             assert np.array_equal(u[k], v[k])
         assert u[3]["iter"] == v[3]["iter"] == 40
+
+
+def test_warm_start_from_database():
+    """Data-driven warm start: GPU solutions at three neighbouring states,
+    combined by WarmStartDB at the query, start the GPU solve; the iterates match the oracle
+    started from the same point, and the solve needs fewer iterations than cold."""
+    from paper_2406_05846_b200.warmstart import WarmStartDB
+    N, q = 5, (0.6, 1.0)
+    db = WarmStartDB()
+    for st in ((0.5, 0.8), (0.75, 1.0), (0.55, 1.3)):
+        g = make(compile_relaxation(models.pendulum(N, *st)))
+        ok, _ = g.solve(1e-6, 20000)
+        assert ok
+        X, y, Sg, _ = g.get()
+        db.add(st, X, y, Sg)
+    sdp = compile_relaxation(models.pendulum(N, *q))
+    start = db.query(q)
+    g = make(sdp)
+    g.set_start(*start)
+    o = Oracle(sdp)
+    o.set_start(*start)
+    g.iterate(20); o.iterate(20)
+    _compare(g, o, 1e-9, "db-warm")
+    cold, warm = make(sdp), make(sdp)
+    warm.set_start(*start)
+    ok_c, it_c = cold.solve(1e-5, 20000)
+    ok_w, it_w = warm.solve(1e-5, 20000)
+    assert ok_c and ok_w and it_w < it_c, (it_w, it_c)
