@@ -35,10 +35,13 @@ def case(name):
                "pend30": lambda: models.pendulum(30, 0.1, 0.0),
                "synth": lambda: models.synthetic_shape("small", 6, seed=1),
                "toy": lambda: models.toy(4),
+               "pend5k1": lambda: (models.pendulum(5, 0.3, 1.0), 1),
+               "toyk1": lambda: (models.toy(4), 1),
                "wide190": lambda: models.synthetic_shape("wide190", 2, seed=2),
                "wide231": lambda: models.synthetic_shape("wide231", 2, seed=3),
                "cartpole": lambda: models.synthetic_shape("cartpole", 3, seed=4)}[name]()
-        _CACHE[name] = compile_relaxation(pop)
+        pop, kappa = pop if isinstance(pop, tuple) else (pop, 2)   # kappa = 1: App. B (NEXT-4)
+        _CACHE[name] = compile_relaxation(pop, kappa=kappa)
     return _CACHE[name]
 
 
@@ -140,7 +143,8 @@ def _compare(g, o, tol, tag):
 
 
 @pytest.mark.parametrize("name,sigma,tau", [("pend5", 1.0, 1.618), ("synth", 0.5, 1.95),
-                                            ("toy", 2.0, 1.0), ("pend3", 1.0, 1.618)])
+                                            ("toy", 2.0, 1.0), ("pend3", 1.0, 1.618),
+                                            ("pend5k1", 1.0, 1.618), ("toyk1", 1.0, 1.618)])
 def test_50_iterations_parity(name, sigma, tau):
     sdp = case(name)
     g = make(sdp, sigma=sigma, tau=tau, check_every=10)

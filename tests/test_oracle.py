@@ -173,3 +173,18 @@ def test_pendulum_small_certified():
     assert feas
     xi = suboptimality_gap(p_hat, LB)
     assert -1e-9 <= xi < 1e-2
+
+
+def test_relaxation_hierarchy_is_monotone():
+    """Theorem 1: p*_1 <= p*_2 <= p* — the first-order relaxation
+    (App. B variant, kappa = 1) bounds the second-order one from below, both below the
+    brute-force optimum of the toy problem."""
+    N = 3
+    p = []
+    for kappa in (1, 2):
+        o = Oracle(compile_relaxation(models.toy(N=N), kappa=kappa), OracleConfig(sigma=1.0))
+        it, ok = o.solve_to_tol(1e-8, 50000)
+        assert ok, kappa
+        p.append(o.residuals()[3])
+    p_hat = _toy_grid_opt(N)
+    assert p[0] <= p[1] + 1e-6 and p[1] <= p_hat + 1e-6, (p, p_hat)
