@@ -28,6 +28,8 @@ def main():
     ap.add_argument("--every", type=int, default=7)
     ap.add_argument("--tol", type=float, default=1e-6)
     ap.add_argument("--maxiter", type=int, default=60000)
+    ap.add_argument("--balance", action="store_true",
+                    help="residual-balancing sigma policy of bench.py (reading R-new-2) instead of sigma = 1")
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
 
@@ -36,11 +38,12 @@ def main():
     from paper_2406_05846_b200.warmstart import WarmStartDB
     from strom_inputs import compile_relaxation, models
     stream = torch.cuda.Stream()
+    pol = dict(sigma=1.0, sigma_period=20, sigma_ratio=1.5, sigma_factor=1.1) if a.balance else {}
 
     def solve(state, start=None):
         sdp = compile_relaxation(models.pendulum(a.N, *state))
         t0 = time.perf_counter()
-        g = S.StromAdmm(S.StromSdp(sdp), S.strom_admm_default_config(check_every=100), stream=stream)
+        g = S.StromAdmm(S.StromSdp(sdp), S.strom_admm_default_config(check_every=100, **pol), stream=stream)
         if start is not None:
             g.set_start(*start)
         ok, it = g.solve(a.tol, a.maxiter)
@@ -71,7 +74,7 @@ def main():
     def med(key, f):
         v = [r[key][f] for r in rows if r[key]["ok"]]
         return float(np.median(v)) if v else None
-    out = {"N": a.N, "tol": a.tol, "db_states": len(db), "db_build_s": t_db, "queries": len(rows),
+    out = {"N": a.N, "tol": a.tol, "sigma_policy": pol or "fixed sigma = 1", "db_states": len(db), "db_build_s": t_db, "queries": len(rows),
            "cold_ok": sum(r["cold"]["ok"] for r in rows), "warm_ok": sum(r["warm"]["ok"] for r in rows),
            "median_iters": {"cold": med("cold", "iters"), "warm": med("warm", "iters")},
            "median_wall_s": {"cold": med("cold", "wall_s"), "warm": med("warm", "wall_s")},
