@@ -30,6 +30,8 @@ def main():
     ap.add_argument("--maxiter", type=int, default=60000)
     ap.add_argument("--balance", action="store_true",
                     help="residual-balancing sigma policy of bench.py (reading R-new-2) instead of sigma = 1")
+    ap.add_argument("--carry-sigma", action="store_true",
+                    help="start the warm solve at the neighbours' converged sigma (weighted geometric mean)")
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
 
@@ -40,10 +42,11 @@ def main():
     stream = torch.cuda.Stream()
     pol = dict(sigma=1.0, sigma_period=20, sigma_ratio=1.5, sigma_factor=1.1) if a.balance else {}
 
-    def solve(state, start=None):
+    def solve(state, start=None, sigma=None):
         sdp = compile_relaxation(models.pendulum(a.N, *state))
         t0 = time.perf_counter()
-        g = S.StromAdmm(S.StromSdp(sdp), S.strom_admm_default_config(check_every=100, **pol), stream=stream)
+        cfg = dict(pol, sigma=sigma) if sigma is not None else pol
+        g = S.StromAdmm(S.StromSdp(sdp), S.strom_admm_default_config(check_every=100, **cfg), stream=stream)
         if start is not None:
             g.set_start(*start)
         ok, it = g.solve(a.tol, a.maxiter)
@@ -51,15 +54,17 @@ def main():
         wall = time.perf_counter() - t0
         X, y, Sm, _ = g.get()
         r = g.residuals()
-        return {"ok": bool(ok), "iters": int(it), "wall_s": wall,
+        return {"ok": bool(ok), "iters": int(it), "wall_s": wall, "sigma": r["sigma"],
                 "eta": max(r["eta_p"], r["eta_d"], r["eta_g"])}, (X, y, Sm)
 
     db = WarmStartDB()
+    sig = []
     t0 = time.perf_counter()
     for th in np.linspace(0.0, np.pi, a.db_theta):
         for thd in np.linspace(-5.0, 5.0, a.db_dot):
             res, sol = solve((float(th), float(thd)))
             db.add((th, thd), *sol)
+            sig.append(res["sigma"])
     t_db = time.perf_counter() - t0
 
     rows = []
@@ -67,14 +72,18 @@ def main():
         if k % a.every:
             continue
         cold, _ = solve(st)
-        warm, _ = solve(st, db.query(st))
+        s0 = None
+        if a.carry_sigma:
+            idx, w = db.weights(st)
+            s0 = float(np.exp(sum(wi * np.log(sig[i]) for i, wi in zip(idx, w))))
+        warm, _ = solve(st, db.query(st), s0)
         rows.append({"state": list(st), "cold": cold, "warm": warm})
         print(json.dumps(rows[-1]), flush=True)
 
     def med(key, f):
         v = [r[key][f] for r in rows if r[key]["ok"]]
         return float(np.median(v)) if v else None
-    out = {"N": a.N, "tol": a.tol, "sigma_policy": pol or "fixed sigma = 1", "db_states": len(db), "db_build_s": t_db, "queries": len(rows),
+    out = {"N": a.N, "tol": a.tol, "sigma_policy": pol or "fixed sigma = 1", "carry_sigma": a.carry_sigma, "db_states": len(db), "db_build_s": t_db, "queries": len(rows),
            "cold_ok": sum(r["cold"]["ok"] for r in rows), "warm_ok": sum(r["warm"]["ok"] for r in rows),
            "median_iters": {"cold": med("cold", "iters"), "warm": med("warm", "iters")},
            "median_wall_s": {"cold": med("cold", "wall_s"), "warm": med("warm", "wall_s")},
