@@ -1,0 +1,96 @@
+"""Model predictive control closed loop on the pendulum.
+
+"a simulated MPC case starting from theta_0 = 0.1, theta_dot = 0.0. We set the control
+frequency as 10Hz. In almost all time steps, the suboptimality gap is below 1e-2, and the
+average solving time is 0.72s".
+
+Each control step: compile the N-step pendulum SDP at the current state, warm-start it from
+the previous step's (X, y, S) (same block structure, so the iterates transfer entry by entry)
+and its converged sigma, solve on the GPU to eta <= --tol or --maxiter, certify (GPU lower
+bound + GPU extraction + host local solve, paper_2406_05846_b200.certify), apply the first
+control of the certified trajectory z_hat through the discretised dynamics (dt = 0.1 s, one
+model step = one 10 Hz control period) and move to the next state.
+
+  python tools/mpc.py --N 30 --steps 30 --out gpurun_out/mpc.json
+"""
+import argparse
+import json
+import math
+import os
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--N", type=int, default=30)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--theta0", type=float, default=0.1)
+    ap.add_argument("--theta-dot0", type=float, default=0.0)
+    ap.add_argument("--tol", type=float, default=1e-6)
+    ap.add_argument("--maxiter", type=int, default=5000)
+    ap.add_argument("--cold", action="store_true", help="no warm start between control steps")
+    ap.add_argument("--out", default=None)
+    a = ap.parse_args()
+
+    import torch
+    import paper_2406_05846_b200 as S
+    from paper_2406_05846_b200 import certify
+    from strom_inputs import compile_relaxation, models
+    stream = torch.cuda.Stream()
+    pol = dict(sigma_period=20, sigma_ratio=1.5, sigma_factor=1.1)   # reading R-new-2
+
+    th, thd = a.theta0, a.theta_dot0
+    prev, sigma, u_prev = None, 1.0, None
+    rows = []
+    for k in range(a.steps):
+        sdp = compile_relaxation(models.pendulum(a.N, th, thd))
+        dt = sdp.meta["pop"].meta["params"].dt
+        t0 = time.perf_counter()
+        g = S.StromAdmm(S.StromSdp(sdp), S.strom_admm_default_config(check_every=100, sigma=sigma, **pol),
+                        stream=stream)
+        if prev is not None and not a.cold:
+            g.set_start(*prev)
+        ok, it = g.solve(a.tol, a.maxiter)
+        stream.synchronize()
+        t_solve = time.perf_counter() - t0
+        r = g.residuals()
+        lb, _ = g.lower_bound(np.asarray(sdp.R_beta))
+        X, y, Sm, _ = g.get()
+        _, vtop = g.extract()
+        u_start = None if u_prev is None else np.append(u_prev[1:], u_prev[-1])   # shifted plan
+        p_hat, z_hat, feas = certify.pendulum_upper_bound(sdp, X, u_start=u_start, vtop=vtop)
+        xi = certify.suboptimality_gap(p_hat, lb) if feas else float("inf")
+        t_all = time.perf_counter() - t0
+        u_prev = certify.pendulum_controls(z_hat, a.N)
+        rows.append({"step": k, "state": [th, thd], "ok": bool(ok), "iters": int(it),
+                     "eta": max(r["eta_p"], r["eta_d"], r["eta_g"]), "sigma": r["sigma"],
+                     "xi": xi, "u0": float(u_prev[0]), "solve_s": t_solve, "solve_and_cert_s": t_all})
+        print(json.dumps(rows[-1]), flush=True)
+        if not a.cold:
+            prev, sigma = (X, y, Sm), r["sigma"]
+        rc, rs, fc, fs = z_hat[5:9]                                   # x_1 under u_0
+        th, thd = math.atan2(rs, rc) % (2 * math.pi), math.atan2(fs, fc) / dt
+
+    xis = np.array([r["xi"] for r in rows])
+    out = {"N": a.N, "steps": a.steps, "tol": a.tol, "maxiter": a.maxiter, "warm": not a.cold,
+           "start": [a.theta0, a.theta_dot0],
+           "frac_xi_below_1e-2": float(np.mean(xis < 1e-2)),
+           "median_xi": float(np.median(xis)),
+           "mean_solve_s": float(np.mean([r["solve_s"] for r in rows])),
+           "mean_solve_and_cert_s": float(np.mean([r["solve_and_cert_s"] for r in rows])),
+           "mean_iters": float(np.mean([r["iters"] for r in rows])),
+           "final_state": [th, thd], "rows": rows}
+    print(json.dumps({k: v for k, v in out.items() if k != "rows"}))
+    if a.out:
+        os.makedirs(os.path.dirname(a.out) or ".", exist_ok=True)
+        with open(a.out, "w") as f:
+            json.dump(out, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()
