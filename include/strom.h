@@ -165,7 +165,11 @@ strom_status strom_admm_get_device(strom_admm *h, double *dX, double *dy, double
 /* Valid lower bound LB = <b,y> + sum_beta R_beta min(0, lambda_min((C - A*y)_beta))
  * (eq:strom:sgsadmm:valid-lowerbound) at the current y, computed
  * on the device (A*y and an eigenvalues-only Jacobi). R_beta[nblocks] host array
- * (Theorem 2). lambda_min[nblocks] optional output. */
+ * (Theorem 2). lambda_min[nblocks] optional output: the computed
+ * smallest eigenvalue of each block lowered by its error margin 3 n_beta u ||Z_beta||_F
+ * (Z = C - A*y, u = 2^-53), so the bound is never overstated by rounding. EEIG when a
+ * block hit the Jacobi sweep cap (a capped run overestimates lambda_min; no bound is
+ * returned). The iterate and the solver state (done flag, residuals) are unchanged. */
 strom_status strom_admm_lower_bound(strom_admm *h, const double *R_beta, double *lb,
                                     double *lambda_min);
 

@@ -240,6 +240,40 @@ class StromAdmm:
                                     _torch_stream_ptr(stream), idbuf, rank, nranks), "strom_admm_setup")
         self.handle = h
         self.n, self.m = sdp.n, sdp.m
+        self.device, self.stream = device, stream
+
+    def _device_arg(self, t, count: int, what: str):
+        """A torch CUDA tensor handed to the C-ABI as a raw device pointer: float64,
+        contiguous, exactly `count` elements, on the handle's device (the library reads
+        or writes count doubles through it)."""
+        if t is None:
+            return None
+        import torch
+        if not (t.is_cuda and t.device.index == self.device):
+            raise ValueError(f"{what}: tensor must live on cuda:{self.device}")
+        if t.dtype != torch.float64 or not t.is_contiguous() or t.numel() != count:
+            raise ValueError(f"{what}: need a contiguous float64 tensor of {count} elements, got "
+                             f"{t.dtype} {tuple(t.shape)} contiguous={t.is_contiguous()}")
+        return C.c_void_p(int(t.data_ptr()))
+
+    def _order_before(self):
+        """The library copies on the handle's stream: make it wait for the caller's
+        current stream (which produced the tensors)."""
+        import torch
+        cur = torch.cuda.current_stream(self.device)
+        if self.stream is not None:
+            self.stream.wait_stream(cur)
+        else:
+            cur.synchronize()
+
+    def _order_after(self):
+        """... and make the caller's current stream wait for the handle's copies."""
+        import torch
+        cur = torch.cuda.current_stream(self.device)
+        if self.stream is not None:
+            cur.wait_stream(self.stream)
+        else:
+            torch.cuda.synchronize(self.device)
 
     def set_start(self, X=None, y=None, S=None):
         f = lambda a: None if a is None else np.ascontiguousarray(a, dtype=np.float64)
@@ -248,9 +282,10 @@ class StromAdmm:
                       "strom_admm_set_start")
 
     def set_start_device(self, X=None, y=None, S=None):
-        p = lambda t: None if t is None else C.c_void_p(int(t.data_ptr()))
-        return _check(load().strom_admm_set_start_device(self.handle, p(X), p(y), p(S)),
-                      "strom_admm_set_start_device")
+        args = (self._device_arg(X, self.n, "X"), self._device_arg(y, self.m, "y"),
+                self._device_arg(S, self.n, "S"))
+        self._order_before()
+        return _check(load().strom_admm_set_start_device(self.handle, *args), "strom_admm_set_start_device")
 
     def iterate(self, iters: int):
         return _check(load().strom_admm_iterate(self.handle, int(iters)), "strom_admm_iterate")
@@ -271,8 +306,12 @@ class StromAdmm:
         return Xa, ya, Sa, res.as_dict()
 
     def get_device(self, X=None, y=None, S=None):
-        p = lambda t: None if t is None else C.c_void_p(int(t.data_ptr()))
-        return _check(load().strom_admm_get_device(self.handle, p(X), p(y), p(S)), "strom_admm_get_device")
+        args = (self._device_arg(X, self.n, "X"), self._device_arg(y, self.m, "y"),
+                self._device_arg(S, self.n, "S"))
+        self._order_before()          # the caller may still be reading the buffers
+        st = _check(load().strom_admm_get_device(self.handle, *args), "strom_admm_get_device")
+        self._order_after()
+        return st
 
     def residuals(self):
         return self.get(False, False, False)[3]

@@ -608,7 +608,7 @@ __global__ void __launch_bounds__(512, 1) k_eig(EigArgs a) {
       nn = warp_sum(nn);
       const double nr = sqrt(nn);
       if (lane == 0) lamv[j] = nr - s;
-      if (proj) {
+      if (proj || a.mode == 2) {     // mode 2 returns unit eigenvectors (strom.h)
         const double inv = 1.0 / nr;
         for (int i = lane; i < n; i += 32) uj[i] *= inv;
       }
@@ -627,10 +627,13 @@ __global__ void __launch_bounds__(512, 1) k_eig(EigArgs a) {
     return;
   }
   if (!proj) {
+    // eigenvalue error floor for the certificate (PAPER.md:535-537 must never overstate
+    // the bound): lambda_j = ||u_j|| - s carries an absolute error ~ n u (||Z||_F + s) =
+    // 1.5 n u s (s = 2 ||Z||_F); the reported lambda_min is lowered by that margin.
     if (tid == 0) {
       double lm = lam[0];
       for (int k = 1; k < n; ++k) lm = fmin(lm, lam[k]);
-      a.lam_min[bidx] = lm;
+      a.lam_min[bidx] = lm - 1.5 * n * 2.220446049250313e-16 * s;
     }
     return;
   }
@@ -985,10 +988,10 @@ __global__ void __cluster_dims__(kClusterEig, 1, 1) __launch_bounds__(512, 1) k_
     return;
   }
   if (!proj) {
-    if (tid == 0 && crank == 0) {
+    if (tid == 0 && crank == 0) {   // with the same error margin as k_eig
       double lm = lam[0];
       for (int k = 1; k < n; ++k) lm = fmin(lm, lam[k]);
-      a.lam_min[bidx] = lm;
+      a.lam_min[bidx] = lm - 1.5 * n * 2.220446049250313e-16 * s;
     }
     return;
   }

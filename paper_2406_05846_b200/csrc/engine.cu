@@ -1541,14 +1541,21 @@ strom_status strom_admm_extract(strom_admm *h, double *lam12, double *vtop) {
   }
   DevState ds;
   CK(d2h(h, &ds, h->st, sizeof(DevState)));
-  const int32_t done_old = ds.done;
+  const int32_t done_old = ds.done, fail_old = ds.eig_fail;
   const int32_t zero = 0;
   CK(cudaMemcpyAsync(&h->st->done, &zero, sizeof(int32_t), cudaMemcpyHostToDevice, h->stream));
+  CK(cudaMemcpyAsync(&h->st->eig_fail, &zero, sizeof(int32_t), cudaMemcpyHostToDevice, h->stream));
   int nl = 0;
   strom_status st = launch_eig(h, 2, h->y, nl);
   if (st) return st;
+  CK(d2h(h, &ds, h->st, sizeof(DevState)));
   CK(cudaMemcpyAsync(&h->st->done, &done_old, sizeof(int32_t), cudaMemcpyHostToDevice, h->stream));
+  CK(cudaMemcpyAsync(&h->st->eig_fail, &fail_old, sizeof(int32_t), cudaMemcpyHostToDevice, h->stream));
   CK(cudaStreamSynchronize(h->stream));
+  if (ds.eig_fail) {
+    set_error("strom_admm_extract: Jacobi sweep cap reached on block " + std::to_string(ds.eig_fail - 1));
+    return STROM_EEIG;
+  }
   CK(d2h(h, lam12, h->lam12_dev, sizeof(double) * 2 * nb));
   if (vtop) CK(d2h(h, vtop, h->vtop_dev, sizeof(double) * nt));
   return STROM_OK;
@@ -1557,18 +1564,32 @@ strom_status strom_admm_extract(strom_admm *h, double *lam12, double *vtop) {
 strom_status strom_admm_lower_bound(strom_admm *h, const double *R_beta, double *lb, double *lambda_min) {
   if (!h || !R_beta || !lb) { set_error("strom_admm_lower_bound: NULL argument"); return STROM_EINVAL; }
   CK(cudaSetDevice(h->device));
+  DevState ds;
+  CK(d2h(h, &ds, h->st, sizeof(DevState)));
+  const int32_t done_old = ds.done, fail_old = ds.eig_fail;
   const int32_t zero = 0;
   CK(cudaMemcpyAsync(&h->st->done, &zero, sizeof(int32_t), cudaMemcpyHostToDevice, h->stream));
+  CK(cudaMemcpyAsync(&h->st->eig_fail, &zero, sizeof(int32_t), cudaMemcpyHostToDevice, h->stream));
   int nl = 0;
   strom_status st = launch_eig(h, 1, h->y, nl);
   if (st) return st;
   std::vector<double> lam(h->nblocks), yh(h->m), bh(h->m);
   CK(cudaStreamSynchronize(h->stream));
+  CK(d2h(h, &ds, h->st, sizeof(DevState)));
+  const int32_t fail = ds.eig_fail;
+  // the certificate call leaves the solver state as it found it (X_b is scratch)
+  CK(cudaMemcpyAsync(&h->st->done, &done_old, sizeof(int32_t), cudaMemcpyHostToDevice, h->stream));
+  CK(cudaMemcpyAsync(&h->st->eig_fail, &fail_old, sizeof(int32_t), cudaMemcpyHostToDevice, h->stream));
+  if (fail) {
+    // a capped Jacobi run overestimates lambda_min, so no valid bound can be returned
+    set_error("strom_admm_lower_bound: Jacobi sweep cap reached on block " + std::to_string(fail - 1));
+    return STROM_EEIG;
+  }
   CK(d2h(h, lam.data(), h->lam_dev, sizeof(double) * h->nblocks));
   CK(d2h(h, yh.data(), h->y, sizeof(double) * h->m));
   CK(d2h(h, bh.data(), h->b, sizeof(double) * h->m));
-  // <b,y> + sum_beta R_beta min(0, lambda_min); the eigenvalue
-  // backward-error floor n*u*||Z|| keeps the bound valid under rounding.
+  // <b,y> + sum_beta R_beta min(0, lambda_min); lambda_min already
+  // carries the eigenvalue error margin (K-EIG mode 1), so the bound stays valid.
   double by = 0.0;
   for (int i = 0; i < h->m; ++i) by += bh[i] * yh[i];
   double acc = by;

@@ -188,3 +188,94 @@ def test_relaxation_hierarchy_is_monotone():
         p.append(o.residuals()[3])
     p_hat = _toy_grid_opt(N)
     assert p[0] <= p[1] + 1e-6 and p[1] <= p_hat + 1e-6, (p, p_hat)
+
+
+# ---------------------------------------------------------------- KKT residuals (hand values)
+def test_kkt_residuals_hand_values_1x1():
+    """eq:strom:sgsadmm:kkt-residual at a constructed point of the 1x1 SDP
+    min x s.t. x = 1: X = 3, y = 2, S = 0.5 gives, by hand,
+    eta_p = |3 - 1| / (1 + 1) = 1, eta_d = |2 + 0.5 - 1| / (1 + 1) = 0.75,
+    <C,X> = 3, <b,y> = 2, eta_g = |3 - 2| / (1 + 3 + 2) = 1/6."""
+    from oracle import kkt_residuals
+    ep, ed, eg, po, do = kkt_residuals(np.array([3.0]), np.array([1.0]), np.array([2.0]),
+                                       np.array([0.5]), np.array([1.0]), np.array([3.0]),
+                                       np.array([2.0]))
+    assert (ep, ed, po, do) == (1.0, 0.75, 3.0, 2.0)
+    assert abs(eg - 1.0 / 6.0) < 1e-16
+
+
+def test_kkt_residuals_hand_values_2x2_offdiagonal():
+    """Same residuals on a 2x2 block with off-diagonal entries, which fixes the norms as
+    Frobenius norms of the matrices (svec with sqrt2 off-diagonal scaling, PAPER.md:571,
+    reading Q15) and the '1 +' normalisations of PAPER.md:501-508. Row: tr X = 2.
+    X = [[1, .5], [.5, 2]], y = .25, S = [[.5, .75], [.75, 1]], C = [[1, 1], [1, 0]]:
+      A(X) - b = 3 - 2 = 1, eta_p = 1 / (1 + 2) = 1/3;
+      A*y + S - C = [[-.25, -.25], [-.25, 1.25]], ||.||_F^2 = 3 * .0625 + 1.5625 = 1.75,
+      ||C||_F^2 = 3, eta_d = sqrt(1.75) / (1 + sqrt(3));
+      <C,X> = tr(CX) = 1 + 2 * .5 + 0 = 2, <b,y> = .5, eta_g = 1.5 / (1 + 2 + .5) = 3/7."""
+    from oracle import kkt_residuals
+    sdp = H.make_sdp([2], [{(0, 0, 0): 1.0, (0, 1, 1): 1.0}], [2.0], [np.array([[1.0, 1.0], [1.0, 0.0]])])
+    o = Oracle(sdp)
+    X = mat_to_svec(np.array([[1.0, 0.5], [0.5, 2.0]]))
+    S = mat_to_svec(np.array([[0.5, 0.75], [0.75, 1.0]]))
+    y = np.array([0.25])
+    ep, ed, eg, po, do = kkt_residuals(o.apply_A(X), o.b, o.apply_At(y), S, o.C, X, y)
+    assert abs(ep - 1.0 / 3.0) < 1e-15
+    assert abs(ed - sqrt(1.75) / (1.0 + sqrt(3.0))) < 1e-15
+    assert abs(po - 2.0) < 1e-15 and do == 0.5
+    assert abs(eg - 3.0 / 7.0) < 1e-15
+
+
+def test_kkt_residuals_vanish_at_closed_form_optimum():
+    """At the exact primal-dual optimum of the 1x1 SDP (x = 1, y = 1, S = 0) every
+    residual is zero; moving X alone changes eta_p and eta_g but not eta_d (eta_d
+    involves only the dual pair)."""
+    from oracle import kkt_residuals
+    one = np.array([1.0])
+    assert kkt_residuals(one, one, one, np.zeros(1), one, one, one) == (0.0, 0.0, 0.0, 1.0, 1.0)
+    ep, ed, eg, _, _ = kkt_residuals(2 * one, one, one, np.zeros(1), one, 2 * one, one)
+    assert ep > 0 and eg > 0 and ed == 0.0
+
+
+# ---------------------------------------------------------------- sigma policy (reading Q2)
+def test_sigma_rule_period_and_clamp_hand_sequence():
+    """Reading Q2 (PAPER.md:454 only says sigma > 0): every `sigma_period` completed
+    iterations, eta_d > ratio * eta_x -> sigma * factor; eta_x > ratio * eta_d ->
+    sigma / factor; otherwise unchanged; clamped to [sigma_min, sigma_max]. Hand sequence
+    (period 5, ratio 2, factor 1.5, clamp [0.5, 3])."""
+    from oracle import sigma_update
+    cfg = OracleConfig(sigma_period=5, sigma_ratio=2.0, sigma_factor=1.5, sigma_min=0.5, sigma_max=3.0)
+    assert sigma_update(1.0, 4, 10.0, 1.0, cfg) == 1.0          # not a multiple of the period
+    assert sigma_update(1.0, 5, 10.0, 1.0, cfg) == 1.5          # eta_d dominates: raise
+    assert sigma_update(1.5, 10, 1.0, 10.0, cfg) == 1.0         # eta_x dominates: lower
+    assert sigma_update(1.0, 15, 1.0, 1.9, cfg) == 1.0          # within the ratio band
+    assert sigma_update(2.5, 20, 10.0, 1.0, cfg) == 3.0         # clamped above
+    assert sigma_update(0.6, 25, 1.0, 10.0, cfg) == 0.5         # clamped below
+    assert sigma_update(2.0, 25, 1.0, 10.0, OracleConfig(sigma_period=0)) == 2.0   # fixed sigma
+
+
+def test_sigma_raises_dual_feasibility():
+    """The premise of the rule's direction: sigma is the penalty on the dual constraint
+    A*y + S = C (the augmented Lagrangian of PAPER.md:447-449), so a larger sigma makes
+    that constraint's residual eta_d smaller and the primal-side residual eta_x larger."""
+    sdp = compile_relaxation(models.pendulum(3, 0.3, 1.0))
+    lo, hi = Oracle(sdp, OracleConfig(sigma=0.05)), Oracle(sdp, OracleConfig(sigma=20.0))
+    lo.iterate(30); hi.iterate(30)
+    assert hi.trace.eta_d[-1] < lo.trace.eta_d[-1] / 10
+    assert hi.trace.eta_x[-1] > lo.trace.eta_x[-1]
+
+
+def test_sigma_balancing_beats_fixed_and_reversed():
+    """From a badly scaled sigma_0 the balancing rule reaches eta <= 1e-6 in fewer iterations
+    than keeping sigma_0 fixed; the same rule with the direction reversed (factor < 1) does
+    not converge at all. A sign error in the rule fails this test."""
+    sdp = compile_relaxation(models.pendulum(3, 0.3, 1.0))
+    pol = dict(sigma_period=10, sigma_ratio=1.5, sigma_factor=1.2)
+    runs = {}
+    for name, s0, kw, cap in (("policy_lo", 0.02, pol, 1500), ("fixed_lo", 0.02, {}, 1500),
+                              ("reversed_lo", 0.02, dict(pol, sigma_factor=1 / 1.2), 1500),
+                              ("policy_hi", 50.0, pol, 1500), ("fixed_hi", 50.0, {}, 1500)):
+        o = Oracle(sdp, OracleConfig(sigma=s0, **kw))
+        runs[name] = o.solve_to_tol(1e-6, cap)
+    assert runs["policy_lo"][1] and not runs["fixed_lo"][1] and not runs["reversed_lo"][1], runs
+    assert runs["policy_hi"][1] and runs["fixed_hi"][1] and runs["policy_hi"][0] < runs["fixed_hi"][0], runs
