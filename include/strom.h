@@ -217,6 +217,15 @@ strom_status strom_debug_solve(strom_admm *h, const double *r, double *y);
  * factorisation without a GPU; never used by the iteration). */
 strom_status strom_debug_host_solve(const strom_sdp *sdp, const strom_admm_config *cfg,
                                     const double *r, double *y);
+/* Host execution of the horizon-partitioned solve for rank `rank` of
+ * `nranks` (CPU test of the partition logic, e.g. under a gloo process group). nB (out,
+ * nullable) = number of boundary separator rows. send != NULL: the rank's partial boundary
+ * right-hand side u~_B^r (nB doubles) for y = (eps I + AA*)^{-1} r; recv && y: from the
+ * summed u~_B (recv, nB) the rank's rows of y (caller numbering; rows the rank does not
+ * hold are 0, boundary rows carry the replicated y_B). r is the full right-hand side. */
+strom_status strom_debug_host_part(const strom_sdp *sdp, const strom_admm_config *cfg, int32_t nranks,
+                                   int32_t rank, const double *r, double *send, const double *recv,
+                                   double *y, int32_t *nB);
 /* eps actually used by a handle. */
 double strom_debug_eps(const strom_admm *h);
 /* In-process "virtual ranks": nranks handles of the same SDP on one device play the

@@ -32,6 +32,7 @@ EXPORTS = [
     "strom_admm_factor_info", "strom_admm_kernel_times", "strom_nccl_get_unique_id", "strom_last_error", "strom_version",
     "strom_debug_project_psd", "strom_debug_spmv", "strom_debug_solve", "strom_debug_host_solve",
     "strom_debug_eps", "strom_debug_link_virtual", "strom_debug_iterate_virtual",
+    "strom_debug_host_part",
 ]
 
 
@@ -110,6 +111,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "strom_debug_solve": (I32, [VP, P(D), P(D)]),
         "strom_debug_host_solve": (I32, [VP, P(strom_admm_config), P(D), P(D)]),
         "strom_debug_eps": (D, [VP]),
+        "strom_debug_host_part": (I32, [VP, P(strom_admm_config), I32, I32, P(D), P(D), P(D), P(D), P(I32)]),
         "strom_debug_link_virtual": (I32, [P(VP), I32, VP]),
         "strom_debug_iterate_virtual": (I32, [P(VP), I32, I64]),
     }
@@ -201,6 +203,27 @@ class StromSdp:
         y = np.zeros(self.m)
         _check(load().strom_debug_host_solve(self.handle, C.byref(cfg), _dptr(r), _dptr(y)),
                "strom_debug_host_solve")
+        return y
+
+    def host_part(self, nranks: int, rank: int, r: np.ndarray, recv: Optional[np.ndarray] = None,
+                  cfg: Optional[strom_admm_config] = None):
+        """strom_debug_host_part (test hook): without `recv`, the rank's partial boundary
+        right-hand side (nB doubles); with `recv` (the summed partials), the rank's rows of y."""
+        cfg = cfg or strom_admm_default_config()
+        r = np.ascontiguousarray(r, dtype=np.float64)
+        nB = C.c_int32()
+        lib = load()
+        _check(lib.strom_debug_host_part(self.handle, C.byref(cfg), nranks, rank, _dptr(r), None, None, None,
+                                         C.byref(nB)), "strom_debug_host_part")
+        if recv is None:
+            send = np.zeros(nB.value)
+            _check(lib.strom_debug_host_part(self.handle, C.byref(cfg), nranks, rank, _dptr(r), _dptr(send),
+                                             None, None, None), "strom_debug_host_part")
+            return send
+        recv = np.ascontiguousarray(recv, dtype=np.float64)
+        y = np.zeros(self.m)
+        _check(lib.strom_debug_host_part(self.handle, C.byref(cfg), nranks, rank, _dptr(r), None, _dptr(recv),
+                                         _dptr(y), None), "strom_debug_host_part")
         return y
 
     def __del__(self):

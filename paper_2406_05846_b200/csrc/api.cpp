@@ -60,6 +60,25 @@ strom_status strom_debug_host_solve(const strom_sdp *sdp, const strom_admm_confi
   return STROM_OK;
 }
 
+strom_status strom_debug_host_part(const strom_sdp *sdp, const strom_admm_config *cfg, int32_t nranks,
+                                   int32_t rank, const double *r, double *send, const double *recv,
+                                   double *y, int32_t *nB) {
+  if (!sdp || !cfg || !r) { strom::set_error("strom_debug_host_part: NULL argument"); return STROM_EINVAL; }
+  strom::Factor f;
+  strom_status st = strom::build_factor(sdp->s, cfg->eps_rel, cfg->eps, f);
+  if (st != STROM_OK) return st;
+  strom::PartPlan p;
+  if ((st = strom::make_plan(sdp->s, f, nranks, rank, p)) != STROM_OK) return st;
+  if (nB) *nB = p.nB;
+  if (!send && !(recv && y)) return STROM_OK;
+  if ((st = strom::host_factor_dense(f)) != STROM_OK) return st;
+  strom::PartFactor pf;
+  if ((st = strom::host_factor_partition(f, p, pf)) != STROM_OK) return st;
+  if (send) strom::host_part_begin(f, p, pf, r, send);
+  if (recv && y) strom::host_part_end(f, p, pf, r, recv, y);
+  return STROM_OK;
+}
+
 void strom_admm_default_config(strom_admm_config *cfg) {
   if (!cfg) return;
   std::memset(cfg, 0, sizeof(*cfg));

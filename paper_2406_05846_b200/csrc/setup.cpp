@@ -300,6 +300,11 @@ strom_status build_factor(const Sdp &s, double eps_rel, double eps_abs, Factor &
       if (it == groups.end()) { groups[root] = {i}; group_order.push_back(root); }
       else it->second.push_back(i);
     }
+  // groups in stage order (a leaf row lies in one block, so in one stage): the leaf rows
+  // of a contiguous stage range are contiguous, as the horizon partition needs
+  std::stable_sort(group_order.begin(), group_order.end(), [&](int32_t x, int32_t y) {
+    return owner[groups[x][0]] < owner[groups[y][0]];
+  });
   std::vector<std::vector<int32_t>> leaf_groups;
   std::vector<std::vector<double>> leaf_kinv;
   std::vector<char> is_leaf(m, 0);
@@ -325,6 +330,9 @@ strom_status build_factor(const Sdp &s, double eps_rel, double eps_abs, Factor &
     f.goff.push_back((int64_t)f.gKinv.size());
   }
   f.nL = (int32_t)f.perm.size();
+  f.L_off.assign(P + 1, f.nL);
+  for (int l = f.nL - 1; l >= 0; --l) f.L_off[owner[f.perm[l]]] = l;
+  for (int k = P - 1; k >= 0; --k) f.L_off[k] = std::min(f.L_off[k], f.L_off[k + 1]);
   f.R_off.assign(P + 1, 0);
   std::vector<std::vector<int32_t>> Rrows(P), Srows(std::max(P - 1, 0));
   for (int i = 0; i < m; ++i) {
