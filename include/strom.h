@@ -115,13 +115,20 @@ void strom_admm_default_config(strom_admm_config *cfg);
  * everything to `device`. `cuda_stream` is a cudaStream_t (NULL = the handle creates its
  * own), e.g. a torch.cuda.Stream().cuda_stream.
  * Multi-GPU (nranks > 1, one process per GPU, every rank passes the same SDP and the same
- * 128-byte NCCL unique id from strom_nccl_get_unique_id on rank 0): the PSD projection --
- * the step that "dominates the runtime" and that the paper distributes over GPUs
- * -- is split by contiguous stage ranges balanced by sum n_beta^3; after
- * K-EIG every rank's S and X_b segments are exchanged with NCCL broadcasts captured in the
- * iteration graph; the rest of the iteration is replicated (identical on every rank), so
- * strom_admm_get returns the full iterate on every rank. EINVAL if nranks > 1 without an
- * id or nranks > number of stages; ENCCL on communicator errors.
+ * 128-byte NCCL unique id from strom_nccl_get_unique_id on rank 0): horizon partition
+ * (the paper distributes the moment blocks over GPUs).
+ * Rank r owns the contiguous stage range [cut_r, cut_{r+1}) (balanced by sum n_beta^3):
+ * its blocks (K-EIG, the X update), leaf and interior rows and the separators between its
+ * stages. The separator S_j at a cut couples two ranks; each rank eliminates its own rows
+ * down to these boundary separators, so a solve needs ONE sum over ranks (NCCL allreduce)
+ * of the boundary right-hand side, after which every rank solves the small reduced
+ * boundary system redundantly; a third allreduce per iteration carries the boundary rows'
+ * A X partials and the six residual sums, so every rank takes the same eta / sigma /
+ * termination decision. The three allreduces are captured in the iteration graph.
+ * strom_admm_get / get_device / lower_bound / extract are collective on a partitioned
+ * handle (every rank calls them; they gather the iterate and return it in full on every
+ * rank). EINVAL if nranks > 1 without an id or nranks > number of stages; ENCCL on
+ * communicator errors.
  * Starts cold: X = S = 0 (reading Q13). */
 strom_status strom_admm_setup(strom_admm **out, const strom_sdp *sdp, const strom_admm_config *cfg,
                               int device, void *cuda_stream, const void *nccl_unique_id,
@@ -228,9 +235,12 @@ strom_status strom_debug_host_part(const strom_sdp *sdp, const strom_admm_config
                                    double *y, int32_t *nB);
 /* eps actually used by a handle. */
 double strom_debug_eps(const strom_admm *h);
-/* In-process "virtual ranks": nranks handles of the same SDP on one device play the
- * ranks of the multi-GPU mode; the exchange is a device-to-device copy instead of NCCL.
- * link: partition the projection; iterate: `iters` lock-step iterations of all handles. */
+/* In-process "virtual ranks": nranks handles of the same SDP on one device, made by
+ * strom_debug_setup_virtual (rank r of nranks), play the ranks of the multi-GPU mode with
+ * the same kernels; each sum over ranks is a device kernel instead of an NCCL allreduce.
+ * link: register the peers; iterate: `iters` lock-step iterations of all handles. */
+strom_status strom_debug_setup_virtual(strom_admm **out, const strom_sdp *sdp, const strom_admm_config *cfg,
+                                       int device, void *cuda_stream, int rank, int nranks);
 strom_status strom_debug_link_virtual(strom_admm **handles, int32_t nranks, const strom_sdp *sdp);
 strom_status strom_debug_iterate_virtual(strom_admm **handles, int32_t nranks, int64_t iters);
 

@@ -32,7 +32,7 @@ EXPORTS = [
     "strom_admm_factor_info", "strom_admm_kernel_times", "strom_nccl_get_unique_id", "strom_last_error", "strom_version",
     "strom_debug_project_psd", "strom_debug_spmv", "strom_debug_solve", "strom_debug_host_solve",
     "strom_debug_eps", "strom_debug_link_virtual", "strom_debug_iterate_virtual",
-    "strom_debug_host_part",
+    "strom_debug_host_part", "strom_debug_setup_virtual",
 ]
 
 
@@ -113,6 +113,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "strom_debug_eps": (D, [VP]),
         "strom_debug_host_part": (I32, [VP, P(strom_admm_config), I32, I32, P(D), P(D), P(D), P(D), P(I32)]),
         "strom_debug_link_virtual": (I32, [P(VP), I32, VP]),
+        "strom_debug_setup_virtual": (I32, [P(VP), VP, P(strom_admm_config), C.c_int, VP, C.c_int, C.c_int]),
         "strom_debug_iterate_virtual": (I32, [P(VP), I32, I64]),
     }
     for name, (res, args) in sig.items():
@@ -248,10 +249,13 @@ class StromAdmm:
     """strom_admm_setup and friends on one device / stream."""
 
     def __init__(self, sdp: StromSdp, cfg: Optional[strom_admm_config] = None, device: int = 0,
-                 stream=None, rank: int = 0, nranks: int = 1, nccl_id: Optional[bytes] = None):
+                 stream=None, rank: int = 0, nranks: int = 1, nccl_id: Optional[bytes] = None,
+                 virtual: bool = False):
         """nranks > 1: one process per GPU, the same SDP and the same `nccl_id`
         (strom_nccl_get_unique_id() on rank 0, broadcast by the caller) on every rank;
-        the PSD projection is distributed by stage ranges."""
+        the chain is partitioned along the horizon.
+        virtual=True (tests): rank `rank` of `nranks` in-process ranks on one device
+        (strom_debug_setup_virtual; link them with strom_debug_link_virtual)."""
         lib = load()
         self.sdp = sdp
         self.cfg = cfg or strom_admm_default_config()
@@ -259,8 +263,12 @@ class StromAdmm:
         idbuf = None
         if nccl_id is not None:
             idbuf = C.create_string_buffer(bytes(nccl_id), 128)
-        _check(lib.strom_admm_setup(C.byref(h), sdp.handle, C.byref(self.cfg), device,
-                                    _torch_stream_ptr(stream), idbuf, rank, nranks), "strom_admm_setup")
+        if virtual:
+            _check(lib.strom_debug_setup_virtual(C.byref(h), sdp.handle, C.byref(self.cfg), device,
+                                                 _torch_stream_ptr(stream), rank, nranks), "strom_debug_setup_virtual")
+        else:
+            _check(lib.strom_admm_setup(C.byref(h), sdp.handle, C.byref(self.cfg), device,
+                                        _torch_stream_ptr(stream), idbuf, rank, nranks), "strom_admm_setup")
         self.handle = h
         self.n, self.m = sdp.n, sdp.m
         self.device, self.stream = device, stream

@@ -45,7 +45,6 @@ using namespace strom;
 
 namespace {
 
-constexpr int kWarp = 32;
 constexpr int kGemvChunk = 8;       // vectors per warp in the dedup GEMV
 
 // Programmatic dependent launch: a kernel launched with programmatic stream
@@ -151,11 +150,14 @@ __device__ __forceinline__ double cta_dot(const double *__restrict__ a, const do
 __global__ void k_solve_p1(SolveDev d, RhsArgs ra, const DevState *st) {
   pdl_enter();
   if (st->done) return;
-  const int qi = blockIdx.x * blockDim.x + threadIdx.x;
-  if (qi >= d.nQ) return;
+  // the handle's Q rows: interiors [R_lo, R_hi), then separators [Sl_lo, Sl_hi)
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  const int nRl = d.R_hi - d.R_lo;
+  const int q = idx < nRl ? d.R_lo + idx : d.Sl_lo + (idx - nRl);
+  if (q >= (idx < nRl ? d.R_hi : d.Sl_hi)) return;
+  const int qi = q - d.nL;
   const double is = 1.0 / st->sigma;
   const bool usew = ra.w && st->w_valid;
-  const int q = d.nL + qi;
   double wq;
   double s = rhs(ra, is, q, usew, wq);
   if (ra.wout) ra.wout[q] = wq;
@@ -243,16 +245,22 @@ __global__ void __launch_bounds__(256) k_solve_p3(SolveDev d, const DevState *st
   if (st->done) return;
   const int lane = threadIdx.x & 31;
   const int nw = (gridDim.x * blockDim.x) >> 5;
-  for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < d.nS; w += nw) {
-    const int s = d.S0 + w;
+  for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < d.Sl_hi - d.Sl_lo; w += nw) {
+    const int s = d.Sl_lo + w;
     int j = 0;
     while (j + 1 < d.P - 1 && d.S_off[j + 1] <= s) ++j;   // separator block of s
     const int c = s - d.S_off[j];
-    // stage j: its right separator is S_j -> column wl_j + c; stage j+1: left -> column c
-    const int u0 = d.stage_uid[j], n0 = d.uid_n[u0];
-    const int u1 = d.stage_uid[j + 1], n1 = d.uid_n[u1];
-    const double a0 = warp_dot(d.Ht[u0] + (int64_t)(d.stage_wl[j] + c) * n0, d.u + d.R_off[j], 0, n0, lane);
-    const double a1 = warp_dot(d.Ht[u1] + (int64_t)c * n1, d.u + d.R_off[j + 1], 0, n1, lane);
+    // stage j: its right separator is S_j -> column wl_j + c; stage j+1: left -> column c.
+    // A boundary separator gets only the contribution of the handle's own stage.
+    double a0 = 0.0, a1 = 0.0;
+    if (j >= d.stage_lo && j < d.stage_hi) {
+      const int u0 = d.stage_uid[j], n0 = d.uid_n[u0];
+      a0 = warp_dot(d.Ht[u0] + (int64_t)(d.stage_wl[j] + c) * n0, d.u + d.R_off[j], 0, n0, lane);
+    }
+    if (j + 1 >= d.stage_lo && j + 1 < d.stage_hi) {
+      const int u1 = d.stage_uid[j + 1], n1 = d.uid_n[u1];
+      a1 = warp_dot(d.Ht[u1] + (int64_t)c * n1, d.u + d.R_off[j + 1], 0, n1, lane);
+    }
     if (lane == 0) d.u[s] -= a0 + a1;
   }
 }
@@ -265,20 +273,20 @@ __global__ void __launch_bounds__(256) k_solve_p3(SolveDev d, const DevState *st
 // 64 partial sums to Tpart[X][Y]; the CTA that delivers the last partial of block X
 // (arrival counter) sums them in Y order (deterministic) and re-arms the counter.
 constexpr int kSepTile = 64;
-__global__ void __launch_bounds__(256) k_sep_tri(SolveDev d, int mode, const double *in, double *out,
+__global__ void __launch_bounds__(256) k_sep_tri(TriTiles d, int mode, const double *in, double *out,
                                                  const DevState *st) {
   pdl_enter();
   if (st->done) return;
   __shared__ double colp[8][kSepTile];
   __shared__ int last;
-  const int b = blockIdx.x, nT = d.nTt;
+  const int b = blockIdx.x, nT = d.nT;
   int I = (int)((sqrtf(8.0f * (float)b + 1.0f) - 1.0f) * 0.5f);
   while (I * (I + 1) / 2 > b) --I;
   while ((I + 1) * (I + 2) / 2 <= b) ++I;
   const int J = b - I * (I + 1) / 2;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int n = d.nS;
-  const double *Tt = d.Ttile + (int64_t)b * kSepTile * kSepTile;
+  const int n = d.n;
+  const double *Tt = d.tile + (int64_t)b * kSepTile * kSepTile;
   const int X = mode == 0 ? I : J;          // block this tile contributes to
   const int Y = mode == 0 ? J : I;          // block of the input it reads
   double t0[8], t1[8];
@@ -288,7 +296,7 @@ __global__ void __launch_bounds__(256) k_sep_tri(SolveDev d, int mode, const dou
     t0[k] = __ldg(Tt + r * kSepTile + lane);
     t1[k] = __ldg(Tt + r * kSepTile + lane + 32);
   }
-  double *P = d.Tpart + ((int64_t)X * nT + Y) * kSepTile;
+  double *P = d.part + ((int64_t)X * nT + Y) * kSepTile;
   if (mode == 0) {
     const int j0 = J * kSepTile + lane, j1 = j0 + 32;
     const double x0 = j0 < n ? in[j0] : 0.0, x1 = j1 < n ? in[j1] : 0.0;
@@ -322,7 +330,7 @@ __global__ void __launch_bounds__(256) k_sep_tri(SolveDev d, int mode, const dou
   __threadfence();
   __syncthreads();
   const int need = mode == 0 ? X + 1 : nT - X;   // partials of block X
-  if (threadIdx.x == 0) last = atomicAdd(&d.Tcnt[X], 1u) == (unsigned)(need - 1);
+  if (threadIdx.x == 0) last = atomicAdd(&d.cnt[X], 1u) == (unsigned)(need - 1);
   __syncthreads();
   if (!last) return;
   __threadfence();
@@ -330,10 +338,10 @@ __global__ void __launch_bounds__(256) k_sep_tri(SolveDev d, int mode, const dou
     const int i = X * kSepTile + threadIdx.x;
     const int y0 = mode == 0 ? 0 : X, y1 = mode == 0 ? X + 1 : nT;
     double v = 0.0;
-    for (int yb = y0; yb < y1; ++yb) v += __ldcg(d.Tpart + ((int64_t)X * nT + yb) * kSepTile + threadIdx.x);
+    for (int yb = y0; yb < y1; ++yb) v += __ldcg(d.part + ((int64_t)X * nT + yb) * kSepTile + threadIdx.x);
     if (i < n) out[i] = v;
   }
-  if (threadIdx.x == 0) d.Tcnt[X] = 0u;
+  if (threadIdx.x == 0) d.cnt[X] = 0u;
 }
 
 // setup: lower 64x64 tiles of the lower-triangular matrix C (column-major nS x nS)
@@ -357,10 +365,10 @@ __global__ void k_solve_p6a(SolveDev d, const int32_t *row_stage, double *y, con
   pdl_enter();
   if (st->done) return;
   const int lane = threadIdx.x & 31, nw = (gridDim.x * blockDim.x) >> 5;
-  const int nR = d.S0 - d.nL;
+  const int nR = d.R_hi - d.R_lo;
   for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nR; w += nw) {
-  const int q = d.nL + w;
-  const int k = row_stage[w];
+  const int q = d.R_lo + w;
+  const int k = row_stage[q - d.nL];
   const int uid = d.stage_uid[k], wk = d.uid_w[uid], wl = d.stage_wl[k];
   const int i = q - d.R_off[k];
   const double *Hi = d.H[uid] + (int64_t)i * wk;
@@ -378,8 +386,8 @@ __global__ void k_solve_p6a(SolveDev d, const int32_t *row_stage, double *y, con
 __global__ void k_solve_p7(SolveDev d, RhsArgs ra, double *y, const DevState *st) {
   pdl_enter();
   if (st->done) return;
-  const int l = blockIdx.x * blockDim.x + threadIdx.x;
-  if (l >= d.nL) return;
+  const int l = d.L_lo + blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= d.L_hi) return;
   const double is = 1.0 / st->sigma;
   const bool usew = ra.w && st->w_valid;
   const int g = d.leaf_group[l], g0 = d.gptr[g], gs = d.gptr[g + 1] - g0, a = l - g0;
@@ -418,25 +426,49 @@ __global__ void k_spmv(int m, const int64_t *rp, const int32_t *ci, const double
   y[i] = sparse_dot(rp, ci, v, x, i);
 }
 
+// Rows of k_spmv_ax: three ranges (leaves, interiors, separators) of the handle.
+struct AxRows {
+  int32_t L_lo, L_hi, R_lo, R_hi, S_lo, S_hi;
+  // horizon partition: boundary rows hold partial row dots; they go to send[] at compact
+  // offsets (left boundary [lb_lo, lb_hi) -> lb_c.., right [rb_lo, rb_hi) -> rb_c..) and
+  // are left out of this rank's residual sums (k_finalize_dist adds them after the sum)
+  double *send; int32_t nB, lb_lo, lb_hi, lb_c, rb_lo, rb_hi, rb_c;
+  __device__ int row(int idx, int &ok) const {
+    const int nl = L_hi - L_lo, nr = R_hi - R_lo, ns = S_hi - S_lo;
+    ok = idx < nl + nr + ns;
+    return idx < nl ? L_lo + idx : (idx < nl + nr ? R_lo + idx - nl : S_lo + idx - nl - nr);
+  }
+};
+
 // AX = A X^{k+1}; partials ||AX - b||^2, <b, y>  (Step 4 residuals).
 // The last CTA to finish (arrival ticket) reduces every CTA's partials and those of
-// k_update in a fixed order and runs finalize_state (no separate reduction launch).
-__device__ void finalize_state(const double *part_ax, int nax, const double *part_up, int nup, DevState *st);
-__global__ void k_spmv_ax(int m, const int64_t *rp, const int32_t *ci, const double *v, const double *x,
+// k_update in a fixed order and runs finalize_state (no separate reduction launch); with a
+// horizon partition it writes the rank's six partial sums after the boundary partials in
+// send[] instead (the sum over ranks and finalize_state follow in k_finalize_dist).
+__device__ void reduce_partials(const double *part_ax, int nax, const double *part_up, int nup, double (&acc)[6]);
+__device__ void finalize_scalars(const double (&acc)[6], DevState *st);
+__global__ void k_spmv_ax(AxRows rows, const int64_t *rp, const int32_t *ci, const double *v, const double *x,
                           double *ax, const double *b, const double *y, double *part, const double *part_up,
                           int nup, DevState *st) {
   pdl_enter();
   if (st->done) return;
   __shared__ double red[2 * 32];
   __shared__ int last;
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  int ok;
+  const int i = rows.row(blockIdx.x * blockDim.x + threadIdx.x, ok);
   double acc[2] = {0.0, 0.0};
-  if (i < m) {
+  if (ok) {
     const double s = sparse_dot(rp, ci, v, x, i);
     ax[i] = s;
-    const double d = s - b[i];
-    acc[0] = d * d;
-    acc[1] = b[i] * y[i];
+    if (rows.send && i >= rows.lb_lo && i < rows.lb_hi) {
+      rows.send[rows.lb_c + i - rows.lb_lo] = s;
+    } else if (rows.send && i >= rows.rb_lo && i < rows.rb_hi) {
+      rows.send[rows.rb_c + i - rows.rb_lo] = s;
+    } else {
+      const double d = s - b[i];
+      acc[0] = d * d;
+      acc[1] = b[i] * y[i];
+    }
   }
   block_sum<2>(acc, red);
   if (threadIdx.x == 0) {
@@ -447,21 +479,30 @@ __global__ void k_spmv_ax(int m, const int64_t *rp, const int32_t *ci, const dou
   __syncthreads();
   if (!last) return;
   __threadfence();
-  finalize_state(part, (int)gridDim.x, part_up, nup, st);
-  if (threadIdx.x == 0) st->ticket = 0;
+  double tot[6];
+  reduce_partials(part, (int)gridDim.x, part_up, nup, tot);
+  if (threadIdx.x == 0) {
+    if (rows.send) {
+      for (int k = 0; k < 6; ++k) rows.send[rows.nB + k] = tot[k];
+    } else {
+      finalize_scalars(tot, st);
+    }
+    st->ticket = 0;
+  }
 }
 
-// Step 4: X^{k+1} = X + tau sigma (S + A*y - C) (eq:strom:sgsadmm:solve-X); partials
-// ||S + A*y - C||^2, <C, X^{k+1}>, ||X^{k+1}||^2, ||X^{k+1} - Pi(X_b)||^2.
-__global__ void k_update(int64_t n, const int64_t *Atp, const int32_t *Atr, const double *Atv,
+// Step 4: X^{k+1} = X + tau sigma (S + A*y - C) (eq:strom:sgsadmm:solve-X) on svec entries
+// [j0, j0 + cnt); partials ||S + A*y - C||^2, <C, X^{k+1}>, ||X^{k+1}||^2, ||X^{k+1} - Pi(X_b)||^2.
+__global__ void k_update(int64_t j0, int64_t cnt, const int64_t *Atp, const int32_t *Atr, const double *Atv,
                          const double *y, double *X, const double *S, const double *C, const double *Xb,
                          double *part, const DevState *st) {
   pdl_enter();
   if (st->done) return;
   __shared__ double red[4 * 32];
-  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t jl = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
-  if (j < n) {
+  if (jl < cnt) {
+    const int64_t j = j0 + jl;
     const double aty = sparse_dot(Atp, Atr, Atv, y, j);
     const double sigma = st->sigma, tau = st->tau;
     const double rd = S[j] + aty - C[j];
@@ -479,39 +520,119 @@ __global__ void k_update(int64_t n, const int64_t *Atp, const int32_t *Atr, cons
     for (int k = 0; k < 4; ++k) part[4 * blockIdx.x + k] = acc[k];
 }
 
-// eta, sigma policy (reading Q2), termination; run by the last CTA of
-// k_spmv_ax with all of its threads
-__device__ void finalize_state(const double *part_ax, int nax, const double *part_up, int nup, DevState *st) {
+// Fixed-order reduction of the per-CTA partials of k_spmv_ax (2 each) and k_update (4 each)
+// by all threads of one CTA; valid in thread 0: ||AX-b||^2, <b,y>, ||A*y+S-C||^2, <C,X>,
+// ||X||^2, ||X - Pi(X_b)||^2.
+__device__ void reduce_partials(const double *part_ax, int nax, const double *part_up, int nup, double (&acc)[6]) {
   __shared__ double red[6 * 32];
-  double acc[6] = {0, 0, 0, 0, 0, 0};
+  for (int k = 0; k < 6; ++k) acc[k] = 0.0;
   for (int b = threadIdx.x; b < nax; b += blockDim.x) {
     acc[0] += __ldcg(part_ax + 2 * b); acc[1] += __ldcg(part_ax + 2 * b + 1);
   }
   for (int b = threadIdx.x; b < nup; b += blockDim.x)
     for (int k = 0; k < 4; ++k) acc[2 + k] += __ldcg(part_up + 4 * b + k);
   block_sum<6>(acc, red);
-  if (threadIdx.x == 0) {
-    const double eta_p = sqrt(acc[0]) / (1.0 + st->normb);
-    const double eta_d = sqrt(acc[2]) / (1.0 + st->normC);
-    const double pobj = acc[3], dobj = acc[1];
-    const double eta_g = fabs(pobj - dobj) / (1.0 + fabs(pobj) + fabs(dobj));
-    const double eta_x = sqrt(acc[5]) / (1.0 + sqrt(acc[4]));
-    st->eta_p = eta_p; st->eta_d = eta_d; st->eta_g = eta_g;
-    st->pobj = pobj; st->dobj = dobj; st->eta_x = eta_x;
-    st->sigma_used = st->sigma;
-    if (!isfinite(eta_p) || !isfinite(eta_d) || !isfinite(eta_g)) st->nan_flag = 1;
-    st->iter += 1;
-    if (st->sigma_period > 0 && (st->iter % st->sigma_period) == 0) {
-      double sg = st->sigma;
-      if (eta_d > st->sigma_ratio * eta_x) sg = fmin(sg * st->sigma_factor, st->sigma_max);
-      else if (eta_x > st->sigma_ratio * eta_d) sg = fmax(sg / st->sigma_factor, st->sigma_min);
-      st->sigma = sg;
-    }
-    const double eta = fmax(eta_p, fmax(eta_d, eta_g));
-    st->eig_warm_valid = 1;   // every block's eigenbasis was stored by this iteration
-    st->w_valid = 1;          // Step 3 stored AC - A S^{k+1} for every row
-    if ((st->tol >= 0.0 && eta <= st->tol) || st->nan_flag) st->done = 1;
+}
+
+// eta, sigma policy (reading Q2), termination; thread 0 only
+__device__ void finalize_scalars(const double (&acc)[6], DevState *st) {
+  const double eta_p = sqrt(acc[0]) / (1.0 + st->normb);
+  const double eta_d = sqrt(acc[2]) / (1.0 + st->normC);
+  const double pobj = acc[3], dobj = acc[1];
+  const double eta_g = fabs(pobj - dobj) / (1.0 + fabs(pobj) + fabs(dobj));
+  const double eta_x = sqrt(acc[5]) / (1.0 + sqrt(acc[4]));
+  st->eta_p = eta_p; st->eta_d = eta_d; st->eta_g = eta_g;
+  st->pobj = pobj; st->dobj = dobj; st->eta_x = eta_x;
+  st->sigma_used = st->sigma;
+  if (!isfinite(eta_p) || !isfinite(eta_d) || !isfinite(eta_g)) st->nan_flag = 1;
+  st->iter += 1;
+  if (st->sigma_period > 0 && (st->iter % st->sigma_period) == 0) {
+    double sg = st->sigma;
+    if (eta_d > st->sigma_ratio * eta_x) sg = fmin(sg * st->sigma_factor, st->sigma_max);
+    else if (eta_x > st->sigma_ratio * eta_d) sg = fmax(sg / st->sigma_factor, st->sigma_min);
+    st->sigma = sg;
   }
+  const double eta = fmax(eta_p, fmax(eta_d, eta_g));
+  st->eig_warm_valid = 1;   // every block's eigenbasis was stored by this iteration
+  st->w_valid = 1;          // Step 3 stored AC - A S^{k+1} for every row
+  if ((st->tol >= 0.0 && eta <= st->tol) || st->nan_flag) st->done = 1;
+}
+
+// ---- horizon partition (partition.cpp) -------------------------------
+// u~_B^r = u_B - W^T u_I on the adjacent boundary rows, 0 on the others: this rank's term of
+// the one sum over ranks per solve. One warp per boundary row.
+__global__ void k_part_rhs(SolveDev d, PartDev p, const DevState *st) {
+  if (st->done) return;
+  const int lane = threadIdx.x & 31, nw = (gridDim.x * blockDim.x) >> 5;
+  for (int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < p.nB; c += nw) {
+    double v = 0.0;
+    if (c >= p.adj_lo && c < p.adj_hi) {
+      const double dot = p.nI > 0 ? warp_dot(p.Wt + (int64_t)(c - p.adj_lo) * p.nI, d.u + d.S0 + p.I0, 0, p.nI, lane)
+                                  : 0.0;
+      v = d.u[d.S0 + p.Bmap[c]] - dot;
+    }
+    if (lane == 0) p.send[c] = v;
+  }
+}
+
+// after the sum and y_B = L~^{-T} L~^{-1} u~_B: y on every boundary row (replicated), and
+// y_I = T_II^{-1} u_I - W y_B,adj on the internal separators. One warp per row.
+__global__ void k_part_back(SolveDev d, PartDev p, double *y, const DevState *st) {
+  if (st->done) return;
+  const int lane = threadIdx.x & 31, nw = (gridDim.x * blockDim.x) >> 5;
+  for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < p.nB + p.nI; w += nw) {
+    if (w < p.nB) {
+      if (lane == 0) y[d.S0 + p.Bmap[w]] = p.yB[w];
+    } else {
+      const int i = w - p.nB, wb = p.adj_hi - p.adj_lo;
+      const double dot = warp_dot(p.W + (int64_t)i * wb, p.yB + p.adj_lo, 0, wb, lane);
+      if (lane == 0) y[d.S0 + p.I0 + i] = p.zI[i] - dot;
+    }
+  }
+}
+
+// after the sum of the residual payload: full A X on the boundary rows (kept on the owner
+// rank, zeroed on the other so that b - AX enters each right-hand side once), their
+// residual terms, then eta / sigma / termination identically on every rank.
+__global__ void k_finalize_dist(const double *recv, int nB, const int32_t *Bmap, int S0, int own_lo, int own_hi,
+                                int nonown_lo, int nonown_hi, const double *bfull, const double *y, double *ax,
+                                DevState *st) {
+  if (st->done) return;
+  __shared__ double red[2 * 32];
+  double acc2[2] = {0.0, 0.0};
+  for (int c = threadIdx.x; c < nB; c += blockDim.x) {
+    const int i = S0 + Bmap[c];
+    const double full = recv[c], d = full - bfull[i];
+    acc2[0] += d * d;
+    acc2[1] += bfull[i] * y[i];
+    if (c >= own_lo && c < own_hi) ax[i] = full;
+    else if (c >= nonown_lo && c < nonown_hi) ax[i] = 0.0;
+  }
+  block_sum<2>(acc2, red);
+  if (threadIdx.x == 0) {
+    double acc[6];
+    for (int k = 0; k < 6; ++k) acc[k] = recv[nB + k];
+    acc[0] += acc2[0];
+    acc[1] += acc2[1];
+    finalize_scalars(acc, st);
+  }
+}
+
+// zero x outside the owned row ranges (set_start on a partitioned handle)
+__global__ void k_keep_rows(int m, int a0, int a1, int b0, int b1, int c0, int c1, double *x) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const bool keep = (i >= a0 && i < a1) || (i >= b0 && i < b1) || (i >= c0 && i < c1);
+  if (!keep) x[i] = 0.0;
+}
+
+// in-process virtual ranks: recv = sum over ranks of send (fixed rank order)
+__global__ void k_sum_ranks(const double *const *sends, int nranks, int len, double *recv) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= len) return;
+  double v = 0.0;
+  for (int q = 0; q < nranks; ++q) v += sends[q][i];
+  recv[i] = v;
 }
 
 __global__ void k_permute(int m, const int32_t *perm, const double *src, double *dst, int inverse) {
@@ -564,14 +685,31 @@ struct strom_admm {
   std::vector<int> eig_class_np;
   std::vector<int> eig_class_n;              // max block order in the class
   int eig_main_class = 0;                    // class with the largest n^3 work
-  // multi-GPU ("we distribute moment matrices for eig"): rank r projects the
-  // blocks of a contiguous stage range; the S and X_b segments are exchanged after K-EIG.
+  // Multi-GPU horizon partition: rank r owns the stages
+  // [plan.cut[r], plan.cut[r+1]) -- their blocks (K-EIG, update), rows and the factor
+  // pieces -- and the ranks exchange three sums per iteration (the boundary right-hand
+  // side of each solve and the residual payload). Vectors stay full length on every rank;
+  // each rank only works on its ranges.
   int rank = 0, nranks = 1;
   int xfer = 0;                              // 0 single, 1 NCCL ranks, 2 in-process virtual ranks
   ncclComm_t comm = nullptr;
-  cudaEvent_t eig_done_ev = nullptr, copy_done_ev = nullptr;
-  std::vector<int64_t> seg_off, seg_cnt;     // svec segment owned by each rank
-  std::vector<int32_t> stage_cut;            // rank r owns stages [cut[r], cut[r+1])
+  bool part = false;                         // horizon partition active (nranks > 1)
+  PartPlan plan;
+  std::vector<PartPlan> plans;               // every rank's plan (gathers in get())
+  PartDev pd{};
+  TriTiles sep_tiles{};                      // one GPU: the separator L_T^{-1} tiles
+  int64_t *Amp = nullptr; int32_t *Amc = nullptr; double *Amv = nullptr;  // A on own columns
+  double *b_full = nullptr;                  // b in internal order (b is masked to owned rows)
+  double *send3 = nullptr, *recv3 = nullptr; // residual payload: nB boundary A X partials + 6 sums
+  AxRows axrows{};
+  int64_t own_off = 0, own_cnt = 0;          // svec segment of the own blocks
+  std::vector<int64_t> seg_off, seg_cnt;     // svec segment of every rank
+  cudaStream_t stream3 = nullptr;            // fork for the internal-separator solve
+  cudaEvent_t ev3f = nullptr, ev3j = nullptr;
+  // in-process virtual ranks (tests): peers and the exchange bookkeeping
+  std::vector<strom_admm *> peers;
+  const double **sends_dev = nullptr, **sends3_dev = nullptr;
+  cudaEvent_t ev_send = nullptr, ev_used = nullptr;
   std::vector<int32_t *> eig_class_dev_all;  // every block (lower bound, single rank)
   std::vector<std::vector<int32_t>> eig_class_all;
   cudaStream_t stream2 = nullptr;            // fork for concurrent eig size classes
@@ -595,8 +733,11 @@ struct strom_admm {
     if (fork_ev) cudaEventDestroy(fork_ev);
     if (sfork_ev) cudaEventDestroy(sfork_ev);
     if (sjoin_ev) cudaEventDestroy(sjoin_ev);
-    if (eig_done_ev) cudaEventDestroy(eig_done_ev);
-    if (copy_done_ev) cudaEventDestroy(copy_done_ev);
+    if (ev3f) cudaEventDestroy(ev3f);
+    if (ev3j) cudaEventDestroy(ev3j);
+    if (ev_send) cudaEventDestroy(ev_send);
+    if (ev_used) cudaEventDestroy(ev_used);
+    if (stream3) cudaStreamDestroy(stream3);
     if (comm) ncclCommDestroy(comm);
     if (join_ev) cudaEventDestroy(join_ev);
     if (stream2) cudaStreamDestroy(stream2);
@@ -695,56 +836,112 @@ bool use_pdl(const strom_admm *h, int edge) {
   return (mask & edge) && !h->prof_capture && h->xfer == 0;
 }
 
-strom_status launch_solve(strom_admm *h, const RhsArgs &ra, double *y, int &nl, bool pdl_first = false) {
-  // P1 -> { main: P2 (v = L^{-1} u), P6' (w = L^{-T} v) | fork: P3 (u_S -= H^T u_R), P4, P5 }
-  //    -> join -> P6'' (y_R = w - H y_S) -> P7. Critical path 6 kernels.
+// Front half of one solve y = (eps I + AA*)^{-1} r (K-TRSV):
+//   P1 -> { main: P2 (v = L^{-1} u), P6' (w = L^{-T} v) | fork: P3 (u_S -= H^T u_R), separators }
+// One GPU: the separator solve P4, P5 (L_T^{-1} tiles) completes the fork here.
+// Horizon partition: the fork ends with this rank's boundary term u~_B^r in pd.send (the
+// sum over ranks follows), and a third stream solves the internal separators z_I.
+strom_status launch_solve_front(strom_admm *h, const RhsArgs &ra, double *y, int &nl, bool pdl_first) {
   const SolveDev &d = h->sd;
   cudaStream_t s = h->stream;
   const int TB = 256;
   nl = 0;
-  const int nR = d.S0 - d.nL;
-  if (d.nQ > 0) {
+  const int nRl = d.R_hi - d.R_lo, nSl = d.Sl_hi - d.Sl_lo;
+  if (nRl + nSl > 0) {
     mark(h, "trsv_p1_leaf_fwd");
-    CK(launch_k(use_pdl(h, kPdlP1) && pdl_first, k_solve_p1, (d.nQ + TB - 1) / TB, TB, 0, s, d, ra, (const DevState *)h->st));
+    CK(launch_k(use_pdl(h, kPdlP1) && pdl_first, k_solve_p1, (nRl + nSl + TB - 1) / TB, TB, 0, s, d, ra,
+                (const DevState *)h->st));
     ++nl;
   }
-  const bool fork = d.nS > 0 && h->stream2;
+  const bool fork = nSl > 0 && h->stream2;
   if (fork) {
     CK(cudaEventRecord(h->sfork_ev, s));
     CK(cudaStreamWaitEvent(h->stream2, h->sfork_ev, 0));
   }
-  if (d.nS > 0) {
+  if (nSl > 0) {
     cudaStream_t s2 = fork ? h->stream2 : s;
-    k_solve_p3<<<std::min((d.nS + 7) / 8, 4 * h->num_sms), 256, 0, s2>>>(d, h->st); ++nl;
-    const int ntl = d.nTt * (d.nTt + 1) / 2;
-    k_sep_tri<<<ntl, 256, 0, s2>>>(d, 0, d.u + d.S0, d.z + d.S0, h->st); ++nl;
-    k_sep_tri<<<ntl, 256, 0, s2>>>(d, 1, d.z + d.S0, y + d.S0, h->st); ++nl;
+    k_solve_p3<<<std::min((nSl + 7) / 8, 4 * h->num_sms), 256, 0, s2>>>(d, h->st); ++nl;
+    if (!h->part) {
+      const TriTiles &T = h->sep_tiles;
+      const int ntl = T.nT * (T.nT + 1) / 2;
+      k_sep_tri<<<ntl, 256, 0, s2>>>(T, 0, d.u + d.S0, d.z + d.S0, h->st); ++nl;
+      k_sep_tri<<<ntl, 256, 0, s2>>>(T, 1, d.z + d.S0, y + d.S0, h->st); ++nl;
+    } else {
+      const PartDev &p = h->pd;
+      if (p.nI > 0) {            // z_I = T_II^{-1} u_I on a third stream, overlapping the sum
+        CK(cudaEventRecord(h->ev3f, s2));
+        CK(cudaStreamWaitEvent(h->stream3, h->ev3f, 0));
+        const int ntl = p.LI.nT * (p.LI.nT + 1) / 2;
+        k_sep_tri<<<ntl, 256, 0, h->stream3>>>(p.LI, 0, d.u + d.S0 + p.I0, p.zI2, h->st);
+        k_sep_tri<<<ntl, 256, 0, h->stream3>>>(p.LI, 1, p.zI2, p.zI, h->st);
+        CK(cudaEventRecord(h->ev3j, h->stream3));
+        nl += 2;
+      }
+      if (p.nB > 0) { k_part_rhs<<<std::min((p.nB + 7) / 8, 2 * h->num_sms), 256, 0, s2>>>(d, p, h->st); ++nl; }
+    }
   }
-  if (h->nitems > 0 && nR > 0) {
+  if (h->nitems > 0 && nRl > 0) {
     const int gg = h->nsingle + ((h->nitems - h->nsingle) * 32 + TB - 1) / TB;
     mark(h, "trsv_p2_stage_Linv");
-    CK(launch_k(use_pdl(h, kPdlP2) && d.nQ > 0, k_gemv_stage, gg, TB, 0, s, d, (const GemvItem *)h->items, h->nitems,
-                h->nsingle, (const int32_t *)h->stage_list, 0, (const double *)d.u, d.v, (const DevState *)h->st));
+    CK(launch_k(use_pdl(h, kPdlP2) && nRl + nSl > 0, k_gemv_stage, gg, TB, 0, s, d, (const GemvItem *)h->items,
+                h->nitems, h->nsingle, (const int32_t *)h->stage_list, 0, (const double *)d.u, d.v,
+                (const DevState *)h->st));
     mark(h, "trsv_p6b_stage_LinvT");
     CK(launch_k(use_pdl(h, kPdlP6b), k_gemv_stage, gg, TB, 0, s, d, (const GemvItem *)h->items, h->nitems, h->nsingle,
-                (const int32_t *)h->stage_list, 1, (const double *)d.v, d.nS > 0 ? d.t : y, (const DevState *)h->st));
+                (const int32_t *)h->stage_list, 1, (const double *)d.v, nSl > 0 ? d.t : y, (const DevState *)h->st));
     nl += 2;
+  }
+  CK(cudaGetLastError());
+  return STROM_OK;
+}
+
+// Back half: (partition: y_B from the summed boundary right-hand side, y_I) -> join ->
+// P6'' (y_R = w - H y_S) -> P7 (leaves).
+strom_status launch_solve_back(strom_admm *h, const RhsArgs &ra, double *y, int &nl) {
+  const SolveDev &d = h->sd;
+  cudaStream_t s = h->stream;
+  const int TB = 256;
+  nl = 0;
+  const int nRl = d.R_hi - d.R_lo, nSl = d.Sl_hi - d.Sl_lo;
+  const bool fork = nSl > 0 && h->stream2;
+  if (h->part && nSl > 0) {
+    const PartDev &p = h->pd;
+    cudaStream_t s2 = fork ? h->stream2 : s;
+    if (p.nB > 0) {
+      const int ntl = p.LB.nT * (p.LB.nT + 1) / 2;
+      k_sep_tri<<<ntl, 256, 0, s2>>>(p.LB, 0, p.recv, p.tB, h->st);
+      k_sep_tri<<<ntl, 256, 0, s2>>>(p.LB, 1, p.tB, p.yB, h->st);
+      nl += 2;
+    }
+    if (p.nI > 0) CK(cudaStreamWaitEvent(s2, h->ev3j, 0));
+    k_part_back<<<std::min((p.nB + p.nI + 7) / 8, 4 * h->num_sms), 256, 0, s2>>>(d, p, y, h->st); ++nl;
   }
   if (fork) {
     CK(cudaEventRecord(h->sjoin_ev, h->stream2));
     CK(cudaStreamWaitEvent(s, h->sjoin_ev, 0));
   }
-  if (nR > 0 && d.nS > 0) {
+  if (nRl > 0 && nSl > 0) {
     mark(h, "trsv_p6a_stage_H");
-    k_solve_p6a<<<std::min((nR * 32 + TB - 1) / TB, 8 * h->num_sms), TB, 0, s>>>(d, h->row_stage_R, y, h->st); ++nl;
+    k_solve_p6a<<<std::min((nRl * 32 + TB - 1) / TB, 8 * h->num_sms), TB, 0, s>>>(d, h->row_stage_R, y, h->st); ++nl;
   }
-  if (d.nL > 0) {
+  const int nLl = d.L_hi - d.L_lo;
+  if (nLl > 0) {
     mark(h, "trsv_p7_leaf_bwd");
-    const bool after_kernel = nR > 0 && d.nS > 0;   // P6'' on this stream just before
-    CK(launch_k(use_pdl(h, kPdlP7) && after_kernel, k_solve_p7, (d.nL + TB - 1) / TB, TB, 0, s, d, ra, y, (const DevState *)h->st));
+    const bool after_kernel = nRl > 0 && nSl > 0;   // P6'' on this stream just before
+    CK(launch_k(use_pdl(h, kPdlP7) && after_kernel, k_solve_p7, (nLl + TB - 1) / TB, TB, 0, s, d, ra, y,
+                (const DevState *)h->st));
     ++nl;
   }
   CK(cudaGetLastError());
+  return STROM_OK;
+}
+
+strom_status launch_solve(strom_admm *h, const RhsArgs &ra, double *y, int &nl, bool pdl_first = false) {
+  int n1 = 0, n2 = 0;
+  strom_status st;
+  if ((st = launch_solve_front(h, ra, y, n1, pdl_first)) != STROM_OK) return st;
+  if ((st = launch_solve_back(h, ra, y, n2)) != STROM_OK) return st;
+  nl = n1 + n2;
   return STROM_OK;
 }
 
@@ -806,113 +1003,85 @@ strom_status launch_eig(strom_admm *h, int mode, const double *yv, int &nl) {
   return STROM_OK;
 }
 
-// Steps 1-2 (solve, projection of the locally owned blocks)
-strom_status launch_iteration_A(strom_admm *h, int &nl_total) {
-  int nl = 0;
-  nl_total = 0;
-  RhsArgs ra{h->b, h->AX, h->AC, h->Arp, h->Aci, h->Av, h->S, h->wrhs, nullptr};
-  strom_status st;
-  if ((st = launch_solve(h, ra, h->yh, nl, true)) != STROM_OK) return st;  // Step 1
-  nl_total += nl;
-  if ((st = launch_eig(h, 0, h->yh, nl)) != STROM_OK) return st;         // Step 2 (A* fused)
-  nl_total += nl;
-  return STROM_OK;
-}
-
-// NCCL exchange of every rank's S and X_b segment (in-place broadcasts, one group)
-strom_status nccl_exchange(strom_admm *h) {
-  if (ncclGroupStart() != ncclSuccess) { set_error("ncclGroupStart"); return STROM_ENCCL; }
-  for (int r = 0; r < h->nranks; ++r) {
-    double *sp = h->S + h->seg_off[r], *xp = h->Xb + h->seg_off[r];
-    if (ncclBroadcast(sp, sp, (size_t)h->seg_cnt[r], ncclDouble, r, h->comm, h->stream) != ncclSuccess ||
-        ncclBroadcast(xp, xp, (size_t)h->seg_cnt[r], ncclDouble, r, h->comm, h->stream) != ncclSuccess) {
-      ncclGroupEnd();
-      set_error("ncclBroadcast of the projection segments failed");
-      return STROM_ENCCL;
-    }
+// The sums over ranks of a partitioned iteration: 0 = the boundary right-hand side of a
+// solve (pd.send -> pd.recv, on the solve's fork stream), 1 = the residual payload
+// (send3 -> recv3). NCCL ranks: one allreduce each, captured in the iteration graph.
+// In-process virtual ranks: the orchestrator (strom_debug_iterate_virtual) sums instead.
+strom_status exchange(strom_admm *h, int which) {
+  if (h->xfer != 1) return STROM_OK;
+  const bool solve = which == 0;
+  const size_t len = solve ? (size_t)h->pd.nB : (size_t)h->pd.nB + 6;
+  if (len == 0) return STROM_OK;
+  cudaStream_t s = solve && h->stream2 && h->sd.Sl_hi > h->sd.Sl_lo ? h->stream2 : h->stream;
+  if (ncclAllReduce(solve ? h->pd.send : h->send3, solve ? h->pd.recv : h->recv3, len, ncclDouble, ncclSum,
+                    h->comm, s) != ncclSuccess) {
+    set_error("ncclAllReduce failed");
+    return STROM_ENCCL;
   }
-  if (ncclGroupEnd() != ncclSuccess) { set_error("ncclGroupEnd"); return STROM_ENCCL; }
   return STROM_OK;
 }
 
-// Steps 3-4 and the residuals
-strom_status launch_iteration_B(strom_admm *h, int &nl_total) {
+// One iteration as segments separated by the sums over ranks:
+//   seg 0  Step 1 solve, front                                      | sum 0
+//   seg 1  Step 1 back, Step 2 (K-EIG, own blocks), Step 3 front   | sum 0
+//   seg 2  Step 3 back, Step 4 update (own segment), A X + partials | sum 1
+//   seg 3  eta, sigma, termination (k_finalize_dist)
+// Unpartitioned handles run segments 0-2 without sums; k_spmv_ax finalises.
+strom_status launch_segment(strom_admm *h, int seg, int &nl) {
   cudaStream_t s = h->stream;
   const int TB = 256;
-  int nl = 0;
-  nl_total = 0;
-  RhsArgs ra{h->b, h->AX, h->AC, h->Arp, h->Aci, h->Av, h->S, nullptr, h->wrhs};
+  nl = 0;
+  int n1 = 0;
   strom_status st;
-  // Step 3: solve with A S^{k+1} formed inside the right-hand side (and kept in wrhs)
-  if ((st = launch_solve(h, ra, h->y, nl)) != STROM_OK) return st;
-  nl_total += nl;
-  // Step 4 + residual partials
-  mark(h, "update_X");
-  CK(launch_k(use_pdl(h, kPdlUpd), k_update, h->nup, TB, 0, s, h->n, (const int64_t *)h->Atp, (const int32_t *)h->Atr,
-              (const double *)h->Atv, (const double *)h->y, h->X, (const double *)h->S, (const double *)h->C,
-              (const double *)h->Xb, h->part_up, (const DevState *)h->st));
-  mark(h, "spmv_AX_resid");
-  CK(launch_k(use_pdl(h, kPdlAx), k_spmv_ax, h->nax, TB, 0, s, h->m, (const int64_t *)h->Arp, (const int32_t *)h->Aci,
-              (const double *)h->Av, (const double *)h->X, h->AX, (const double *)h->b, (const double *)h->y,
-              h->part_ax, (const double *)h->part_up, h->nup, h->st));
-  mark(h, nullptr);
-  nl_total += 2;
-  CK(cudaGetLastError());
+  RhsArgs ra1{h->b, h->AX, h->AC, h->Amp, h->Amc, h->Amv, h->S, h->wrhs, nullptr};   // Step 1
+  RhsArgs ra3{h->b, h->AX, h->AC, h->Amp, h->Amc, h->Amv, h->S, nullptr, h->wrhs};   // Step 3
+  if (seg == 0) return launch_solve_front(h, ra1, h->yh, nl, true);
+  if (seg == 1) {
+    if ((st = launch_solve_back(h, ra1, h->yh, n1)) != STROM_OK) return st;
+    nl += n1;
+    if ((st = launch_eig(h, 0, h->yh, n1)) != STROM_OK) return st;      // Step 2 (A* fused)
+    nl += n1;
+    if ((st = launch_solve_front(h, ra3, h->y, n1, false)) != STROM_OK) return st;   // Step 3
+    nl += n1;
+    return STROM_OK;
+  }
+  if (seg == 2) {
+    if ((st = launch_solve_back(h, ra3, h->y, n1)) != STROM_OK) return st;
+    nl += n1;
+    mark(h, "update_X");
+    CK(launch_k(use_pdl(h, kPdlUpd), k_update, h->nup, TB, 0, s, h->own_off, h->own_cnt, (const int64_t *)h->Atp,
+                (const int32_t *)h->Atr, (const double *)h->Atv, (const double *)h->y, h->X, (const double *)h->S,
+                (const double *)h->C, (const double *)h->Xb, h->part_up, (const DevState *)h->st));
+    mark(h, "spmv_AX_resid");
+    CK(launch_k(use_pdl(h, kPdlAx), k_spmv_ax, h->nax, TB, 0, s, h->axrows, (const int64_t *)h->Amp,
+                (const int32_t *)h->Amc, (const double *)h->Amv, (const double *)h->X, h->AX, (const double *)h->b,
+                (const double *)h->y, h->part_ax, (const double *)h->part_up, h->nup, h->st));
+    mark(h, nullptr);
+    nl += 2;
+    CK(cudaGetLastError());
+    return STROM_OK;
+  }
+  if (seg == 3 && h->part) {
+    const PartPlan &p = h->plan;
+    const int own_lo = p.r < p.R - 1 ? p.B_off[p.r] : 0, own_hi = p.r < p.R - 1 ? p.B_off[p.r + 1] : 0;
+    const int no_lo = p.r > 0 ? p.B_off[p.r - 1] : 0, no_hi = p.r > 0 ? p.B_off[p.r] : 0;
+    k_finalize_dist<<<1, 256, 0, s>>>(h->recv3, p.nB, h->pd.Bmap, h->sd.S0, own_lo, own_hi, no_lo, no_hi,
+                                      h->b_full, h->y, h->AX, h->st);
+    ++nl;
+    CK(cudaGetLastError());
+  }
   return STROM_OK;
 }
 
 strom_status launch_iteration(strom_admm *h, int &nl_total) {
-  int na = 0, nb = 0;
+  nl_total = 0;
+  int nl = 0;
   strom_status st;
-  if ((st = launch_iteration_A(h, na)) != STROM_OK) return st;
-  if (h->xfer == 1 && (st = nccl_exchange(h)) != STROM_OK) return st;
-  if ((st = launch_iteration_B(h, nb)) != STROM_OK) return st;
-  nl_total = na + nb;
-  return STROM_OK;
-}
-
-// Stage ranges balanced by projection work (sum of n^3 over a stage's blocks) and the
-// per-class lists of locally owned blocks. Blocks are stage-sorted, so a rank's blocks
-// (and its svec segment) are contiguous.
-strom_status set_partition(strom_admm *h, const Sdp &s, int rank, int nranks) {
-  const int P = s.nstages;
-  if (nranks < 1 || rank < 0 || rank >= nranks || nranks > P) {
-    set_error("partition: need 1 <= nranks <= number of stages and 0 <= rank < nranks");
-    return STROM_EINVAL;
+  for (int seg = 0; seg < 4; ++seg) {
+    if ((st = launch_segment(h, seg, nl)) != STROM_OK) return st;
+    nl_total += nl;
+    if (h->part && seg < 3 && (st = exchange(h, seg == 2 ? 1 : 0)) != STROM_OK) return st;
   }
-  h->rank = rank; h->nranks = nranks;
-  std::vector<double> cost(P, 1.0);
-  for (int k = 0; k < s.nblocks; ++k) cost[s.bstage[k]] += (double)s.bn[k] * s.bn[k] * s.bn[k];
-  double tot = 0.0;
-  for (double c : cost) tot += c;
-  h->stage_cut.assign(nranks + 1, P);
-  h->stage_cut[0] = 0;
-  double acc = 0.0;
-  int r = 1;
-  for (int k = 0; k < P && r < nranks; ++k) {
-    acc += cost[k];
-    const int left = P - (k + 1);                      // stages still unassigned
-    if (acc >= tot * r / nranks || left == nranks - r) h->stage_cut[r++] = k + 1;
-  }
-  h->seg_off.assign(nranks, 0); h->seg_cnt.assign(nranks, 0);
-  for (int q = 0; q < nranks; ++q) {
-    int b0 = s.nblocks, b1 = 0;
-    for (int k = 0; k < s.nblocks; ++k)
-      if (s.bstage[k] >= h->stage_cut[q] && s.bstage[k] < h->stage_cut[q + 1]) { b0 = std::min(b0, k); b1 = k + 1; }
-    if (b1 > b0) { h->seg_off[q] = s.boff[b0]; h->seg_cnt[q] = s.boff[b1] - s.boff[b0]; }
-  }
-  strom_status st;
-  for (size_t c = 0; c < h->eig_class_all.size(); ++c) {
-    std::vector<int32_t> own;
-    for (int k : h->eig_class_all[c])
-      if (s.bstage[k] >= h->stage_cut[rank] && s.bstage[k] < h->stage_cut[rank + 1]) own.push_back(k);
-    h->eig_class_blocks[c] = own;
-    int32_t *pd = nullptr;
-    if (!own.empty() && (st = h->upload(pd, own))) return st;
-    h->eig_class_dev[c] = pd;
-  }
-  if (!h->eig_done_ev) CK(cudaEventCreateWithFlags(&h->eig_done_ev, cudaEventDisableTiming));
-  if (!h->copy_done_ev) CK(cudaEventCreateWithFlags(&h->copy_done_ev, cudaEventDisableTiming));
   return STROM_OK;
 }
 
@@ -960,7 +1129,51 @@ strom_status reset_state(strom_admm *h) {
 strom_status recompute_products(strom_admm *h) {
   const int TB = 256;
   k_spmv<<<(h->m + TB - 1) / TB, TB, 0, h->stream>>>(h->m, h->Arp, h->Aci, h->Av, h->X, h->AX, nullptr);
+  if (h->part) {   // A X^0 kept on the owned rows only (b - AX enters each right-hand side once)
+    const PartPlan &p = h->plan;
+    k_keep_rows<<<(h->m + TB - 1) / TB, TB, 0, h->stream>>>(h->m, p.leaf_lo, p.leaf_hi, p.R_lo, p.R_hi, p.own_sep_lo,
+                                                            p.own_sep_hi, h->AX);
+  }
   CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(h->stream));
+  return STROM_OK;
+}
+
+// Partitioned handle: make X, S (svec segments) and y (owned rows) of every rank present
+// on this one (collective over the NCCL ranks; device copies between virtual ranks).
+// Only the iteration's own ranges are ever read by the kernels, so this is harmless.
+strom_status gather_full(strom_admm *h) {
+  if (!h->part) return STROM_OK;
+  if (h->xfer == 2 && h->peers.empty()) return STROM_OK;
+  if (h->xfer == 1 && ncclGroupStart() != ncclSuccess) { set_error("ncclGroupStart"); return STROM_ENCCL; }
+  for (int q = 0; q < h->nranks; ++q) {
+    const PartPlan &p = h->plans[q];
+    const std::pair<int64_t, int64_t> segs[2] = {{h->seg_off[q], h->seg_cnt[q]}, {0, 0}};
+    const std::pair<int, int> rows[3] = {{p.leaf_lo, p.leaf_hi}, {p.R_lo, p.R_hi}, {p.own_sep_lo, p.own_sep_hi}};
+    (void)segs;
+    if (h->xfer == 1) {
+      bool ok = ncclBroadcast(h->X + h->seg_off[q], h->X + h->seg_off[q], (size_t)h->seg_cnt[q], ncclDouble, q,
+                              h->comm, h->stream) == ncclSuccess &&
+                ncclBroadcast(h->S + h->seg_off[q], h->S + h->seg_off[q], (size_t)h->seg_cnt[q], ncclDouble, q,
+                              h->comm, h->stream) == ncclSuccess;
+      for (auto &rg : rows)
+        if (rg.second > rg.first)
+          ok = ok && ncclBroadcast(h->y + rg.first, h->y + rg.first, (size_t)(rg.second - rg.first), ncclDouble, q,
+                                   h->comm, h->stream) == ncclSuccess;
+      if (!ok) { ncclGroupEnd(); set_error("ncclBroadcast (gather) failed"); return STROM_ENCCL; }
+    } else if (q != h->rank) {
+      strom_admm *pe = h->peers[q];
+      CK(cudaStreamSynchronize(pe->stream));
+      const size_t bytes = sizeof(double) * (size_t)h->seg_cnt[q];
+      CK(cudaMemcpyAsync(h->X + h->seg_off[q], pe->X + h->seg_off[q], bytes, cudaMemcpyDeviceToDevice, h->stream));
+      CK(cudaMemcpyAsync(h->S + h->seg_off[q], pe->S + h->seg_off[q], bytes, cudaMemcpyDeviceToDevice, h->stream));
+      for (auto &rg : rows)
+        if (rg.second > rg.first)
+          CK(cudaMemcpyAsync(h->y + rg.first, pe->y + rg.first, sizeof(double) * (rg.second - rg.first),
+                             cudaMemcpyDeviceToDevice, h->stream));
+    }
+  }
+  if (h->xfer == 1 && ncclGroupEnd() != ncclSuccess) { set_error("ncclGroupEnd"); return STROM_ENCCL; }
   CK(cudaStreamSynchronize(h->stream));
   return STROM_OK;
 }
@@ -1072,6 +1285,109 @@ strom_status transpose_into(strom_admm *h, int rows, int cols, const double *in,
   return STROM_OK;
 }
 
+// T[rmap[i], cmap[j]] (symmetric, lower triangle valid; column-major nS x nS) -> out
+// (column-major nr x nc)
+__global__ void k_gather_sym(const double *T, int nS, const int32_t *rmap, int nr, const int32_t *cmap, int nc,
+                             double *out) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)nr * nc) return;
+  const int j = (int)(e / nr), i = (int)(e - (int64_t)j * nr);
+  const int a = rmap[i], b = cmap[j];
+  out[e] = a >= b ? T[(int64_t)b * nS + a] : T[(int64_t)a * nS + b];
+}
+
+strom_status alloc_tiles(strom_admm *h, int n, const double *Linv_cm, TriTiles &T) {
+  T.n = n;
+  T.nT = (n + kSepTile - 1) / kSepTile;
+  const int ntiles = T.nT * (T.nT + 1) / 2;
+  double *tiles = nullptr;
+  strom_status st;
+  if ((st = h->alloc(tiles, (size_t)ntiles * kSepTile * kSepTile))) return st;
+  if (n > 0) k_pack_sep_tiles<<<ntiles, 256, 0, h->stream>>>(n, T.nT, Linv_cm, tiles);
+  CK(cudaGetLastError());
+  T.tile = tiles;
+  if ((st = h->alloc(T.part, (size_t)T.nT * T.nT * kSepTile)) || (st = h->alloc(T.cnt, std::max(T.nT, 1)))) return st;
+  CK(cudaMemsetAsync(T.cnt, 0, sizeof(unsigned) * std::max(T.nT, 1), h->stream));
+  return STROM_OK;
+}
+
+// Setup of the horizon-partitioned separator solve (partition.cpp has the math and a host
+// execution): with the full Schur complement T on the device (every rank builds the same
+// global factor), for every rank q: T_II^q -> Cholesky inverse, W^q = (T_II^q)^{-1} T_IB^q
+// (cuBLAS trmm, setup only), and T~ = T_BB - sum_q T_IB^qT W^q; the own rank keeps its
+// tiles and W, every rank keeps the tiles of L~^{-1}.
+strom_status device_partition_factors(strom_admm *h, SolverHandles &H, double *T, int nS, int *dinfo) {
+  const PartPlan &p = h->plan;
+  const int R = p.R, nB = p.nB;
+  strom_status st;
+  std::vector<int32_t> bmap(nB);
+  for (int c = 0; c < nB; ++c) {
+    int b = 0;
+    while (b + 1 < (int)p.B_pos.size() && p.B_off[b + 1] <= c) ++b;
+    bmap[c] = p.B_pos[b] + (c - p.B_off[b]);
+  }
+  int32_t *dB = nullptr;
+  if ((st = h->upload(dB, bmap))) return st;
+  h->pd.Bmap = dB;
+  double *Tt = nullptr;
+  if ((st = h->alloc(Tt, std::max<size_t>((size_t)nB * nB, 1)))) return st;
+  if (nB > 0) k_gather_sym<<<(unsigned)(((int64_t)nB * nB + 255) / 256), 256, 0, h->stream>>>(T, nS, dB, nB, dB, nB, Tt);
+  CK(cudaGetLastError());
+  for (int q = 0; q < R; ++q) {
+    const int ni = p.I1[q] - p.I0[q];
+    const int alo = (q > 0) ? p.B_off[q - 1] : 0, ahi = (q < R - 1) ? p.B_off[q + 1] : nB;
+    const int wb = ahi - alo;
+    if (ni == 0) continue;
+    std::vector<int32_t> imap(ni);
+    for (int i = 0; i < ni; ++i) imap[i] = p.I0[q] + i;
+    int32_t *dI = nullptr;
+    double *A = nullptr, *TIB = nullptr, *Z = nullptr, *W = nullptr;
+    if ((st = h->upload(dI, imap)) || (st = h->alloc(A, (size_t)ni * ni)) || (st = h->alloc(TIB, (size_t)ni * wb)) ||
+        (st = h->alloc(Z, (size_t)ni * wb)) || (st = h->alloc(W, (size_t)ni * wb)))
+      return st;
+    k_gather_sym<<<(unsigned)(((int64_t)ni * ni + 255) / 256), 256, 0, h->stream>>>(T, nS, dI, ni, dI, ni, A);
+    k_gather_sym<<<(unsigned)(((int64_t)ni * wb + 255) / 256), 256, 0, h->stream>>>(T, nS, dI, ni, dB + alo, wb, TIB);
+    CK(cudaGetLastError());
+    if ((st = chol_inverse(H, h->stream, ni, A, dinfo, "an internal separator block"))) return st;
+    const double one = 1.0, mone = -1.0;
+    CBLAS(cublasDtrmm(H.blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, ni, wb,
+                      &one, A, ni, TIB, ni, Z, ni));                 // L^{-1} T_IB
+    CBLAS(cublasDtrmm(H.blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, ni, wb,
+                      &one, A, ni, Z, ni, W, ni));                   // W = L^{-T} L^{-1} T_IB
+    CBLAS(cublasDgemm(H.blas, CUBLAS_OP_T, CUBLAS_OP_N, wb, wb, ni, &mone, TIB, ni, W, ni, &one,
+                      Tt + (int64_t)alo * nB + alo, nB));           // T~[adj, adj] -= T_IB^T W
+    if (q == p.r) {
+      if ((st = alloc_tiles(h, ni, A, h->pd.LI))) return st;
+      h->pd.Wt = W;                                                  // column-major W == row-major W^T
+      double *Wr = nullptr;
+      if ((st = transpose_into(h, wb, ni, W, Wr))) return st;
+      h->pd.W = Wr;
+      CK(cudaStreamSynchronize(h->stream));
+      h->release(A);
+    } else {
+      CK(cudaStreamSynchronize(h->stream));
+      h->release(A); h->release(W);
+    }
+    h->release(TIB); h->release(Z); h->release(dI);
+  }
+  if (nB > 0) {
+    if ((st = chol_inverse(H, h->stream, nB, Tt, dinfo, "the reduced boundary system"))) return st;
+    if ((st = alloc_tiles(h, nB, Tt, h->pd.LB))) return st;
+  }
+  CK(cudaStreamSynchronize(h->stream));
+  h->release(Tt);
+  PartDev &pd = h->pd;
+  pd.nB = nB; pd.adj_lo = p.adj_lo; pd.adj_hi = p.adj_hi;
+  pd.I0 = p.I1[p.r] > p.I0[p.r] ? p.I0[p.r] : 0;
+  pd.nI = p.I1[p.r] - p.I0[p.r];
+  if ((st = h->alloc(pd.send, nB)) || (st = h->alloc(pd.recv, nB)) || (st = h->alloc(pd.tB, nB)) ||
+      (st = h->alloc(pd.yB, nB)) || (st = h->alloc(pd.zI, pd.nI)) || (st = h->alloc(pd.zI2, pd.nI)))
+    return st;
+  CK(cudaMemsetAsync(pd.send, 0, sizeof(double) * std::max(nB, 1), h->stream));
+  CK(cudaMemsetAsync(pd.recv, 0, sizeof(double) * std::max(nB, 1), h->stream));
+  return STROM_OK;
+}
+
 strom_status device_factor_dense(strom_admm *h, std::vector<const double *> &Linv, std::vector<const double *> &LinvT,
                                  std::vector<const double *> &Fp, std::vector<const double *> &Ftp,
                                  std::vector<const double *> &Hp, std::vector<const double *> &Htp,
@@ -1140,6 +1456,12 @@ strom_status device_factor_dense(strom_admm *h, std::vector<const double *> &Lin
       CBLAS(cublasDsyrk(H.blas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, w, un[u], &mone, Fcm[u], un[u], &one,
                         T + (int64_t)off * nS + off, nS));
     }
+    if (h->part) {          // horizon partition: T_II^r, W^r and the reduced boundary system
+      if ((st = device_partition_factors(h, H, T, nS, dinfo))) return st;
+      h->release(T);
+      CK(cudaStreamSynchronize(h->stream));
+      return STROM_OK;
+    }
     if ((st = chol_inverse(H, h->stream, nS, T, dinfo, "the separator Schur complement"))) return st;
     // T holds L_T^{-1} column-major (upper zeroed): pack its lower tiles
     nTt = (nS + kSepTile - 1) / kSepTile;
@@ -1159,12 +1481,18 @@ strom_status device_factor_dense(strom_admm *h, std::vector<const double *> &Lin
 // ============================ C-ABI ===========================================
 extern "C" {
 
-strom_status strom_admm_setup(strom_admm **out, const strom_sdp *sdp_h, const strom_admm_config *cfg,
-                              int device, void *cuda_stream, const void *nccl_unique_id, int rank,
-                              int nranks) {
+}  // extern "C"
+// xfer: 0 one GPU, 1 NCCL ranks, 2 in-process virtual ranks (tests)
+static strom_status setup_impl(strom_admm **out, const strom_sdp *sdp_h, const strom_admm_config *cfg,
+                               int device, void *cuda_stream, const void *nccl_unique_id, int rank,
+                               int nranks, int xfer) {
   if (!out || !sdp_h || !cfg) { set_error("strom_admm_setup: NULL argument"); return STROM_EINVAL; }
   *out = nullptr;
-  if (nranks > 1 && nccl_unique_id == nullptr) {
+  if (nranks < 1 || rank < 0 || rank >= nranks) {
+    set_error("strom_admm_setup: need 0 <= rank < nranks");
+    return STROM_EINVAL;
+  }
+  if (nranks > 1 && xfer == 1 && nccl_unique_id == nullptr) {
     set_error("strom_admm_setup: nranks > 1 needs an NCCL unique id (strom_nccl_get_unique_id)");
     return STROM_EINVAL;
   }
@@ -1192,6 +1520,23 @@ strom_status strom_admm_setup(strom_admm **out, const strom_sdp *sdp_h, const st
   else { CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking)); h->own_stream = true; }
   const Factor &F = h->F;
   const int m = s.m;
+  // ---- horizon partition -------------------------------------
+  h->rank = rank; h->nranks = nranks;
+  h->part = nranks > 1;
+  h->xfer = nranks > 1 ? xfer : 0;
+  if ((st = make_plan(s, F, nranks, rank, h->plan))) return st;
+  h->plans.resize(nranks);
+  for (int q = 0; q < nranks; ++q)
+    if ((st = make_plan(s, F, nranks, q, h->plans[q]))) return st;
+  const PartPlan &pl = h->plan;
+  h->seg_off.assign(nranks, 0); h->seg_cnt.assign(nranks, 0);
+  for (int q = 0; q < nranks; ++q) {
+    int b0 = s.nblocks, b1 = 0;
+    for (int k = 0; k < s.nblocks; ++k)
+      if (s.bstage[k] >= h->plans[q].stage_lo && s.bstage[k] < h->plans[q].stage_hi) { b0 = std::min(b0, k); b1 = k + 1; }
+    if (b1 > b0) { h->seg_off[q] = s.boff[b0]; h->seg_cnt[q] = s.boff[b1] - s.boff[b0]; }
+  }
+  h->own_off = h->seg_off[rank]; h->own_cnt = h->seg_cnt[rank];
   // ---- A in internal row order, A^T by column ------------------------------
   std::vector<int64_t> rp(m + 1, 0);
   for (int i = 0; i < m; ++i) rp[i + 1] = rp[i] + (s.rowptr[F.perm[i] + 1] - s.rowptr[F.perm[i]]);
@@ -1216,9 +1561,31 @@ strom_status strom_admm_setup(strom_admm **out, const strom_sdp *sdp_h, const st
   for (int i = 0; i < m; ++i) bI[i] = s.b[F.perm[i]];
   if ((st = h->upload(h->perm, F.perm)) || (st = h->upload(h->Arp, rp)) || (st = h->upload(h->Aci, ci)) ||
       (st = h->upload(h->Av, av)) || (st = h->upload(h->Atp, cp)) || (st = h->upload(h->Atr, tr)) ||
-      (st = h->upload(h->Atv, tv)) || (st = h->upload(h->C, s.C)) || (st = h->upload(h->b, bI)) ||
+      (st = h->upload(h->Atv, tv)) || (st = h->upload(h->C, s.C)) || (st = h->upload(h->b_full, bI)) ||
       (st = h->upload(h->bn, s.bn)) || (st = h->upload(h->boff, s.boff)))
     return st;
+  if (!h->part) {
+    h->b = h->b_full;
+    h->Amp = h->Arp; h->Amc = h->Aci; h->Amv = h->Av;
+  } else {
+    // A on the own columns only (boundary rows become this rank's partial row dots) and b
+    // on the owned rows only (the right boundary is owned by this rank, the left one not)
+    const int64_t c0 = h->own_off, c1 = h->own_off + h->own_cnt;
+    std::vector<int64_t> mp(m + 1, 0);
+    std::vector<int32_t> mc;
+    std::vector<double> mv;
+    for (int i = 0; i < m; ++i) {
+      for (int64_t t = rp[i]; t < rp[i + 1]; ++t)
+        if (ci[t] >= c0 && ci[t] < c1) { mc.push_back(ci[t]); mv.push_back(av[t]); }
+      mp[i + 1] = (int64_t)mc.size();
+    }
+    std::vector<double> bm(m, 0.0);
+    auto keep = [&](int lo, int hi) { for (int i = lo; i < hi; ++i) bm[i] = bI[i]; };
+    keep(pl.leaf_lo, pl.leaf_hi); keep(pl.R_lo, pl.R_hi); keep(pl.own_sep_lo, pl.own_sep_hi);
+    if ((st = h->upload(h->Amp, mp)) || (st = h->upload(h->Amc, mc)) || (st = h->upload(h->Amv, mv)) ||
+        (st = h->upload(h->b, bm)))
+      return st;
+  }
   if ((st = h->alloc(h->X, s.n)) || (st = h->alloc(h->S, s.n)) || (st = h->alloc(h->Xb, s.n)) ||
       (st = h->alloc(h->y, m)) || (st = h->alloc(h->yh, m)) || (st = h->alloc(h->AX, m)) ||
       (st = h->alloc(h->AC, m)) || (st = h->alloc(h->zeros_m, m)) || (st = h->alloc(h->wrhs, m)) ||
@@ -1233,9 +1600,30 @@ strom_status strom_admm_setup(strom_admm **out, const strom_sdp *sdp_h, const st
   CK(cudaMemset(h->yh, 0, sizeof(double) * m));
   CK(cudaMemset(h->AX, 0, sizeof(double) * m));
   CK(cudaMemset(h->zeros_m, 0, sizeof(double) * m));
+  // AC - A S per row: a partitioned handle writes only its own rows, and the right-hand
+  // sides read it (as 0) for the neighbours' leaf rows its boundary rows couple to
+  CK(cudaMemset(h->wrhs, 0, sizeof(double) * m));
   const int TB = 256;
-  h->nax = (m + TB - 1) / TB;
-  h->nup = (int)((s.n + TB - 1) / TB);
+  // rows of k_spmv_ax and the own svec segment of k_update
+  {
+    AxRows &ar = h->axrows;
+    ar = AxRows{};
+    ar.L_lo = pl.leaf_lo; ar.L_hi = pl.leaf_hi; ar.R_lo = pl.R_lo; ar.R_hi = pl.R_hi;
+    ar.S_lo = pl.sep_lo; ar.S_hi = pl.sep_hi;
+    if (h->part) {
+      if ((st = h->alloc(h->send3, pl.nB + 6)) || (st = h->alloc(h->recv3, pl.nB + 6))) return st;
+      CK(cudaMemset(h->send3, 0, sizeof(double) * (pl.nB + 6)));
+      ar.send = h->send3; ar.nB = pl.nB;
+      ar.lb_lo = ar.lb_hi = ar.rb_lo = ar.rb_hi = 0;
+      if (rank > 0) { ar.lb_lo = pl.sep_lo; ar.lb_hi = pl.own_sep_lo; ar.lb_c = pl.B_off[rank - 1]; }
+      if (rank < nranks - 1) {
+        ar.rb_hi = pl.sep_hi; ar.rb_lo = pl.sep_hi - (pl.B_off[rank + 1] - pl.B_off[rank]); ar.rb_c = pl.B_off[rank];
+      }
+    }
+    const int nrows = (pl.leaf_hi - pl.leaf_lo) + (pl.R_hi - pl.R_lo) + (pl.sep_hi - pl.sep_lo);
+    h->nax = std::max(1, (nrows + TB - 1) / TB);
+    h->nup = (int)std::max<int64_t>(1, (h->own_cnt + TB - 1) / TB);
+  }
   if ((st = h->alloc(h->part_ax, 2 * h->nax)) || (st = h->alloc(h->part_up, 4 * h->nup))) return st;
   // ---- factor upload --------------------------------------------------------
   SolveDev &d = h->sd;
@@ -1259,6 +1647,12 @@ strom_status strom_admm_setup(strom_admm **out, const strom_sdp *sdp_h, const st
   d.G_ptr = p_Gptr; d.G_col = p_Gcol; d.G_val = p_Gval;
   d.Gt_ptr = p_Gtptr; d.Gt_col = p_Gtcol; d.Gt_val = p_Gtval;
   d.R_off = p_Roff; d.S_off = p_Soff; d.stage_uid = p_suid; d.stage_wl = p_swl; d.stage_wr = p_swr;
+  d.L_lo = pl.leaf_lo; d.L_hi = pl.leaf_hi; d.R_lo = pl.R_lo; d.R_hi = pl.R_hi;
+  d.Sl_lo = pl.sep_lo; d.Sl_hi = pl.sep_hi; d.stage_lo = pl.stage_lo; d.stage_hi = pl.stage_hi;
+  CK(cudaStreamCreateWithFlags(&h->stream2, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&h->stream3, cudaStreamNonBlocking));
+  for (cudaEvent_t *e : {&h->fork_ev, &h->join_ev, &h->sfork_ev, &h->sjoin_ev, &h->ev3f, &h->ev3j, &h->ev_send, &h->ev_used})
+    CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   // ---- dense factors: computed on the device (setup only) -------------------------
   const int nu = (int)F.uK.size();
   std::vector<const double *> hLinv(nu), hLinvT(nu), hF(nu), hFt(nu), hH(nu), hHt(nu);
@@ -1272,10 +1666,11 @@ strom_status strom_admm_setup(strom_admm **out, const strom_sdp *sdp_h, const st
       (st = h->upload(p_un, un)) || (st = h->upload(p_uw, uw)))
     return st;
   d.Linv = pp1; d.LinvT = pp2; d.F = pp3; d.Ft = pp4; d.H = pp5; d.Ht = pp6; d.uid_n = p_un; d.uid_w = p_uw;
-  d.Ttile = dTtile; d.nTt = nTt;
+  h->sep_tiles = TriTiles{dTtile, nTt, d.nS, nullptr, nullptr};
   if (nTt > 0) {
-    if ((st = h->alloc(d.Tpart, (size_t)nTt * nTt * kSepTile)) || (st = h->alloc(d.Tcnt, nTt))) return st;
-    CK(cudaMemsetAsync(d.Tcnt, 0, sizeof(unsigned) * nTt, h->stream));
+    if ((st = h->alloc(h->sep_tiles.part, (size_t)nTt * nTt * kSepTile)) || (st = h->alloc(h->sep_tiles.cnt, nTt)))
+      return st;
+    CK(cudaMemsetAsync(h->sep_tiles.cnt, 0, sizeof(unsigned) * nTt, h->stream));
     CK(cudaStreamSynchronize(h->stream));
   }
   if ((st = h->alloc(d.u, m)) || (st = h->alloc(d.v, m)) || (st = h->alloc(d.t, m)) || (st = h->alloc(d.z, m)))
@@ -1292,7 +1687,8 @@ strom_status strom_admm_setup(strom_admm **out, const strom_sdp *sdp_h, const st
   std::vector<GemvItem> items, multi;
   for (int u = 0; u < nu; ++u) {
     std::vector<int32_t> stg;
-    for (int k = 0; k < F.P; ++k) if (F.stage_uid[k] == u && F.R_off[k + 1] > F.R_off[k]) stg.push_back(k);
+    for (int k = pl.stage_lo; k < pl.stage_hi; ++k)       // the own stages only
+      if (F.stage_uid[k] == u && F.R_off[k + 1] > F.R_off[k]) stg.push_back(k);
     // a factor used by one stage with long rows (the first clique's block of the large
     // problems: 14K-18K rows) is streamed with a CTA per row (more bytes in flight)
     static const int cta_rows = [] { const char *e = getenv("STROM_GEMV_CTA_ROWS"); return e ? atoi(e) : 2048; }();
@@ -1341,17 +1737,18 @@ strom_status strom_admm_setup(strom_admm **out, const strom_sdp *sdp_h, const st
       const double w = (double)h->eig_class_blocks[c].size() * nps[c] * nps[c] * nps[c];
       if (w > best) { best = w; h->eig_main_class = (int)c; }
     }
-    CK(cudaStreamCreateWithFlags(&h->stream2, cudaStreamNonBlocking));
-    CK(cudaEventCreateWithFlags(&h->fork_ev, cudaEventDisableTiming));
-    CK(cudaEventCreateWithFlags(&h->join_ev, cudaEventDisableTiming));
-    CK(cudaEventCreateWithFlags(&h->sfork_ev, cudaEventDisableTiming));
-    CK(cudaEventCreateWithFlags(&h->sjoin_ev, cudaEventDisableTiming));
     for (size_t c = 0; c < nps.size(); ++c) {
       int32_t *pd;
       if ((st = h->upload(pd, h->eig_class_blocks[c]))) return st;
-      h->eig_class_dev.push_back(pd);
       h->eig_class_dev_all.push_back(pd);
       h->eig_class_all.push_back(h->eig_class_blocks[c]);
+      std::vector<int32_t> own;                  // K-EIG of the own stages' blocks
+      for (int k : h->eig_class_blocks[c])
+        if (s.bstage[k] >= pl.stage_lo && s.bstage[k] < pl.stage_hi) own.push_back(k);
+      int32_t *po = nullptr;
+      if (!own.empty() && (st = h->upload(po, own))) return st;
+      h->eig_class_blocks[c] = own;
+      h->eig_class_dev.push_back(po);
     }
     size_t maxsm = 0;
     for (int np : nps) maxsm = std::max(maxsm, eig_smem_bytes(np));
@@ -1384,29 +1781,43 @@ strom_status strom_admm_setup(strom_admm **out, const strom_sdp *sdp_h, const st
     CK(h2d(h.get(), h->st, &ds, sizeof(DevState)));
   }
   if ((st = reset_state(h.get()))) return st;
-  k_spmv<<<(m + TB - 1) / TB, TB, 0, h->stream>>>(m, h->Arp, h->Aci, h->Av, h->C, h->AC, nullptr);
+  // A C (partial on the boundary rows of a partitioned handle)
+  k_spmv<<<(m + TB - 1) / TB, TB, 0, h->stream>>>(m, h->Amp, h->Amc, h->Amv, h->C, h->AC, nullptr);
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(h->stream));
-  // ---- multi-GPU: NCCL communicator and the projection partition ----------------
-  if (nranks > 1) {
+  // ---- multi-GPU: NCCL communicator ------------------------------------------------
+  if (h->xfer == 1) {
     ncclUniqueId id;
     std::memcpy(&id, nccl_unique_id, sizeof(id));
     if (ncclCommInitRank(&h->comm, nranks, id, rank) != ncclSuccess) {
       set_error("ncclCommInitRank failed");
       return STROM_ENCCL;
     }
-    if ((st = set_partition(h.get(), s, rank, nranks))) return st;
-    h->xfer = 1;
   }
   // ---- graphs ---------------------------------------------------------------
   h->prof_ev.resize(kMaxProfEvents);
   h->prof_names.assign(kMaxProfEvents, nullptr);
   for (auto &e : h->prof_ev) CK(cudaEventCreate(&e));
-  if ((st = capture(h.get(), h->K, h->graphK, h->execK))) return st;
-  if ((st = capture(h.get(), 1, h->graph1, h->exec1))) return st;
+  if (h->xfer != 2) {        // virtual ranks launch directly (strom_debug_iterate_virtual)
+    if ((st = capture(h.get(), h->K, h->graphK, h->execK))) return st;
+    if ((st = capture(h.get(), 1, h->graph1, h->exec1))) return st;
+  }
   *out = h.release();
   return STROM_OK;
 }
+extern "C" {
+
+strom_status strom_admm_setup(strom_admm **out, const strom_sdp *sdp_h, const strom_admm_config *cfg,
+                              int device, void *cuda_stream, const void *nccl_unique_id, int rank,
+                              int nranks) {
+  return setup_impl(out, sdp_h, cfg, device, cuda_stream, nccl_unique_id, rank, nranks, 1);
+}
+
+strom_status strom_debug_setup_virtual(strom_admm **out, const strom_sdp *sdp_h, const strom_admm_config *cfg,
+                                       int device, void *cuda_stream, int rank, int nranks) {
+  return setup_impl(out, sdp_h, cfg, device, cuda_stream, nullptr, rank, nranks, 2);
+}
+
 
 void strom_admm_destroy(strom_admm *h) { delete h; }
 
@@ -1457,6 +1868,7 @@ extern "C" {
 
 strom_status strom_admm_iterate(strom_admm *h, int64_t iters) {
   if (!h || iters < 0) { set_error("strom_admm_iterate: bad arguments"); return STROM_EINVAL; }
+  if (h->xfer == 2) { set_error("strom_admm_iterate: virtual ranks iterate with strom_debug_iterate_virtual"); return STROM_EINVAL; }
   CK(cudaSetDevice(h->device));
   // iterate() never stops early: clear done and disable tol (fully asynchronous)
   k_set_control<<<1, 1, 0, h->stream>>>(h->st, -1.0);
@@ -1469,6 +1881,7 @@ strom_status strom_admm_iterate(strom_admm *h, int64_t iters) {
 
 strom_status strom_admm_solve(strom_admm *h, double tol, int64_t maxiter, int64_t *iters_done) {
   if (!h || maxiter < 0 || !(tol >= 0.0)) { set_error("strom_admm_solve: bad arguments"); return STROM_EINVAL; }
+  if (h->xfer == 2) { set_error("strom_admm_solve: virtual ranks iterate with strom_debug_iterate_virtual"); return STROM_EINVAL; }
   CK(cudaSetDevice(h->device));
   DevState ds;
   CK(d2h(h, &ds, h->st, sizeof(DevState)));
@@ -1494,6 +1907,10 @@ strom_status strom_admm_solve(strom_admm *h, double tol, int64_t maxiter, int64_
 strom_status strom_admm_get(strom_admm *h, double *X, double *y, double *S, strom_residuals *res) {
   if (!h) { set_error("strom_admm_get: NULL handle"); return STROM_EINVAL; }
   CK(cudaSetDevice(h->device));
+  if (X || y || S) {
+    strom_status gs = gather_full(h);
+    if (gs != STROM_OK) return gs;
+  }
   if (y) k_permute<<<(h->m + 255) / 256, 256, 0, h->stream>>>(h->m, h->perm, h->y, h->tmp_m, 1);
   CK(cudaStreamSynchronize(h->stream));
   CK(cudaGetLastError());
@@ -1517,6 +1934,10 @@ strom_status strom_admm_get(strom_admm *h, double *X, double *y, double *S, stro
 strom_status strom_admm_get_device(strom_admm *h, double *dX, double *dy, double *dS) {
   if (!h) { set_error("strom_admm_get_device: NULL handle"); return STROM_EINVAL; }
   CK(cudaSetDevice(h->device));
+  if (dX || dy || dS) {
+    strom_status gs = gather_full(h);
+    if (gs != STROM_OK) return gs;
+  }
   if (dX) CK(cudaMemcpyAsync(dX, h->X, sizeof(double) * h->n, cudaMemcpyDeviceToDevice, h->stream));
   if (dS) CK(cudaMemcpyAsync(dS, h->S, sizeof(double) * h->n, cudaMemcpyDeviceToDevice, h->stream));
   if (dy) k_permute<<<(h->m + 255) / 256, 256, 0, h->stream>>>(h->m, h->perm, h->y, dy, 1);
@@ -1539,6 +1960,8 @@ strom_status strom_admm_extract(strom_admm *h, double *lam12, double *vtop) {
     if (st == STROM_OK) st = h->alloc(h->vtop_dev, (size_t)nt);
     if (st) return st;
   }
+  strom_status gs = gather_full(h);
+  if (gs != STROM_OK) return gs;
   DevState ds;
   CK(d2h(h, &ds, h->st, sizeof(DevState)));
   const int32_t done_old = ds.done, fail_old = ds.eig_fail;
@@ -1564,6 +1987,8 @@ strom_status strom_admm_extract(strom_admm *h, double *lam12, double *vtop) {
 strom_status strom_admm_lower_bound(strom_admm *h, const double *R_beta, double *lb, double *lambda_min) {
   if (!h || !R_beta || !lb) { set_error("strom_admm_lower_bound: NULL argument"); return STROM_EINVAL; }
   CK(cudaSetDevice(h->device));
+  strom_status gs = gather_full(h);     // partitioned handle: every block's X, y present
+  if (gs != STROM_OK) return gs;
   DevState ds;
   CK(d2h(h, &ds, h->st, sizeof(DevState)));
   const int32_t done_old = ds.done, fail_old = ds.eig_fail;
@@ -1587,7 +2012,7 @@ strom_status strom_admm_lower_bound(strom_admm *h, const double *R_beta, double 
   }
   CK(d2h(h, lam.data(), h->lam_dev, sizeof(double) * h->nblocks));
   CK(d2h(h, yh.data(), h->y, sizeof(double) * h->m));
-  CK(d2h(h, bh.data(), h->b, sizeof(double) * h->m));
+  CK(d2h(h, bh.data(), h->b_full, sizeof(double) * h->m));
   // <b,y> + sum_beta R_beta min(0, lambda_min); lambda_min already
   // carries the eigenvalue error margin (K-EIG mode 1), so the bound stays valid.
   double by = 0.0;
@@ -1636,49 +2061,68 @@ strom_status strom_nccl_get_unique_id(void *id128) {
   return STROM_OK;
 }
 
-// ---- in-process virtual ranks (test harness for the multi-GPU exchange) --------------
+// ---- in-process virtual ranks (test harness for the multi-GPU path) ------------------
+// nranks handles made by strom_debug_setup_virtual (rank r of nranks, one device) play the
+// NCCL ranks: the same segments are launched, and each sum over ranks is a kernel that adds
+// the peers' send buffers in rank order (NCCL's allreduce in the real multi-GPU run).
 strom_status strom_debug_link_virtual(strom_admm **hs, int32_t nranks, const strom_sdp *sdp_h) {
   if (!hs || nranks < 1 || !sdp_h) { set_error("strom_debug_link_virtual: bad arguments"); return STROM_EINVAL; }
-  const Sdp &s = sdp_of(sdp_h);
+  for (int r = 0; r < nranks; ++r)
+    if (!hs[r] || hs[r]->xfer != 2 || hs[r]->nranks != nranks || hs[r]->rank != r) {
+      set_error("strom_debug_link_virtual: handle r must come from strom_debug_setup_virtual(rank r, nranks)");
+      return STROM_EINVAL;
+    }
+  std::vector<const double *> sends(nranks), sends3(nranks);
+  for (int q = 0; q < nranks; ++q) { sends[q] = hs[q]->pd.send; sends3[q] = hs[q]->send3; }
   for (int r = 0; r < nranks; ++r) {
-    strom_status st = set_partition(hs[r], s, r, nranks);
-    if (st) return st;
-    hs[r]->xfer = 2;
+    strom_admm *h = hs[r];
+    h->peers.assign(hs, hs + nranks);
+    strom_status st;
+    if ((st = h->upload(h->sends_dev, sends)) || (st = h->upload(h->sends3_dev, sends3))) return st;
   }
   return STROM_OK;
 }
 
+namespace {
+strom_status exchange_virtual(strom_admm **hs, int R, int which) {
+  const size_t len = which == 0 ? (size_t)hs[0]->pd.nB : (size_t)hs[0]->pd.nB + 6;
+  auto strm = [&](strom_admm *h) {
+    return which == 0 && h->sd.Sl_hi > h->sd.Sl_lo ? h->stream2 : h->stream;
+  };
+  for (int r = 0; r < R; ++r) CK(cudaEventRecord(hs[r]->ev_send, strm(hs[r])));
+  for (int r = 0; r < R; ++r) {
+    strom_admm *h = hs[r];
+    cudaStream_t s = strm(h);
+    for (int q = 0; q < R; ++q) CK(cudaStreamWaitEvent(s, hs[q]->ev_send, 0));
+    if (len > 0)
+      k_sum_ranks<<<(unsigned)((len + 255) / 256), 256, 0, s>>>(which == 0 ? h->sends_dev : h->sends3_dev, R,
+                                                               (int)len, which == 0 ? h->pd.recv : h->recv3);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(h->ev_used, s));
+  }
+  for (int r = 0; r < R; ++r)          // nobody rewrites a send buffer before every rank summed it
+    for (int q = 0; q < R; ++q) {
+      CK(cudaStreamWaitEvent(hs[r]->stream, hs[q]->ev_used, 0));
+      CK(cudaStreamWaitEvent(hs[r]->stream2, hs[q]->ev_used, 0));
+    }
+  return STROM_OK;
+}
+}  // namespace
+
 strom_status strom_debug_iterate_virtual(strom_admm **hs, int32_t nranks, int64_t iters) {
   if (!hs || nranks < 1 || iters < 0) { set_error("strom_debug_iterate_virtual: bad arguments"); return STROM_EINVAL; }
   for (int r = 0; r < nranks; ++r) {
-    const int32_t zero = 0;
-    const double tol = -1.0;
-    CK(cudaMemcpyAsync(&hs[r]->st->done, &zero, sizeof(int32_t), cudaMemcpyHostToDevice, hs[r]->stream));
-    CK(cudaMemcpyAsync(&hs[r]->st->tol, &tol, sizeof(double), cudaMemcpyHostToDevice, hs[r]->stream));
+    if (hs[r]->peers.size() != (size_t)nranks) { set_error("strom_debug_iterate_virtual: link first"); return STROM_EINVAL; }
+    k_set_control<<<1, 1, 0, hs[r]->stream>>>(hs[r]->st, -1.0);
   }
-  for (int64_t it = 0; it < iters; ++it) {
-    int nl;
-    strom_status st;
-    for (int r = 0; r < nranks; ++r) {      // Steps 1-2 on every rank (own blocks only)
-      strom_admm *h = hs[r];
-      for (int q = 0; q < nranks; ++q)        // peers finished reading our last segment
-        if (q != r) CK(cudaStreamWaitEvent(h->stream, hs[q]->copy_done_ev, 0));
-      if ((st = launch_iteration_A(h, nl))) return st;
-      CK(cudaEventRecord(h->eig_done_ev, h->stream));
+  for (int64_t it = 0; it < iters; ++it)
+    for (int seg = 0; seg < 4; ++seg) {
+      int nl;
+      strom_status st;
+      for (int r = 0; r < nranks; ++r)
+        if ((st = launch_segment(hs[r], seg, nl))) return st;
+      if (seg < 3 && (st = exchange_virtual(hs, nranks, seg == 2 ? 1 : 0))) return st;
     }
-    for (int r = 0; r < nranks; ++r) {      // exchange the segments, then Steps 3-4
-      strom_admm *h = hs[r];
-      for (int q = 0; q < nranks; ++q) {
-        if (q == r) continue;
-        CK(cudaStreamWaitEvent(h->stream, hs[q]->eig_done_ev, 0));
-        const size_t bytes = sizeof(double) * (size_t)h->seg_cnt[q];
-        CK(cudaMemcpyAsync(h->S + h->seg_off[q], hs[q]->S + h->seg_off[q], bytes, cudaMemcpyDeviceToDevice, h->stream));
-        CK(cudaMemcpyAsync(h->Xb + h->seg_off[q], hs[q]->Xb + h->seg_off[q], bytes, cudaMemcpyDeviceToDevice, h->stream));
-      }
-      CK(cudaEventRecord(h->copy_done_ev, h->stream));
-      if ((st = launch_iteration_B(h, nl))) return st;
-    }
-  }
   for (int r = 0; r < nranks; ++r) CK(cudaStreamSynchronize(hs[r]->stream));
   return STROM_OK;
 }
@@ -1688,10 +2132,11 @@ double strom_debug_eps(const strom_admm *h) { return h ? h->F.eps : 0.0; }
 // ---- test hooks -----------------------------------------------------------------
 strom_status strom_debug_project_psd(strom_admm *h, const double *Xb, double sigma, double *S_out, double *Pi_out) {
   if (!h || !Xb || !S_out) { set_error("strom_debug_project_psd: NULL argument"); return STROM_EINVAL; }
+  if (h->part) { set_error("strom_debug_project_psd: not available on a partitioned handle"); return STROM_ENOTIMPL; }
   CK(cudaSetDevice(h->device));
   // X_b = X + sigma (A* y - C) with X := Xb_in, y := 0  ->  X_b = Xb_in - sigma C; so
   // feed X := Xb + sigma C is lossy; instead use C := 0 temporarily via tmp buffers.
-  double *Xsave = h->X, *Csave = h->C, *ysave = h->yh;
+  double *Xsave = h->X, *Csave = h->C;
   CK(cudaMemcpyAsync(h->tmp_m, Xb, sizeof(double) * h->n, cudaMemcpyHostToDevice, h->stream));
   CK(cudaMemsetAsync(h->tmp_m2, 0, sizeof(double) * h->n, h->stream));
   DevState ds;
@@ -1704,7 +2149,7 @@ strom_status strom_debug_project_psd(strom_admm *h, const double *Xb, double sig
   h->X = h->tmp_m; h->C = h->tmp_m2;
   int nl = 0;
   strom_status st = launch_eig(h, 0, h->zeros_m, nl);
-  h->X = Xsave; h->C = Csave; (void)ysave;
+  h->X = Xsave; h->C = Csave;
   if (st) return st;
   CK(cudaStreamSynchronize(h->stream));
   CK(d2h(h, S_out, h->S, sizeof(double) * h->n));
@@ -1751,6 +2196,7 @@ strom_status strom_debug_spmv(strom_admm *h, const double *X, double *AX, const 
 
 strom_status strom_debug_solve(strom_admm *h, const double *r, double *y) {
   if (!h || !r || !y) { set_error("strom_debug_solve: NULL argument"); return STROM_EINVAL; }
+  if (h->part) { set_error("strom_debug_solve: not available on a partitioned handle"); return STROM_ENOTIMPL; }
   CK(cudaSetDevice(h->device));
   std::vector<double> ri(h->m);
   for (int i = 0; i < h->m; ++i) ri[i] = r[h->F.perm[i]];

@@ -55,12 +55,30 @@ struct SolveDev {
   const double *const *F; const double *const *Ft;
   const double *const *H; const double *const *Ht;   // H_k = L_k^{-T} F_k (n_k x w), H^T
   const int32_t *uid_n, *uid_w;
-  // separator system: L_T^{-1} (lower nS x nS) as its lower 64x64 tiles (I >= J,
-  // tile-row-major order, each tile row-major, zero padded); per-call partial products
-  // Tpart[X][Y][64] and per-block arrival counters Tcnt[nTt]
-  const double *Ttile; int32_t nTt; double *Tpart; unsigned *Tcnt;
   // work vectors (internal order, length m)
   double *u, *v, *t, *z;
+  // rows this handle works on (internal order). One GPU: everything. Horizon partition
+  // (SURVEY.md §8(e)): the rank's leaves [L_lo, L_hi), interiors [R_lo, R_hi), separators
+  // [Sl_lo, Sl_hi) incl. both boundaries, and its stages [stage_lo, stage_hi).
+  int32_t L_lo, L_hi, R_lo, R_hi, Sl_lo, Sl_hi, stage_lo, stage_hi;
+};
+
+// Lower-triangular inverse (e.g. the separator L_T^{-1}, n x n) stored as its lower 64x64
+// tiles (I >= J, tile-row-major order, each tile row-major, zero padded) for k_sep_tri, with
+// the per-call partial products part[X][Y][64] and per-block arrival counters cnt[nT].
+struct TriTiles {
+  const double *tile; int32_t nT, n; double *part; unsigned *cnt;
+};
+
+// Horizon-partitioned separator solve (partition.cpp) on the device, this rank's pieces.
+struct PartDev {
+  int32_t nB, adj_lo, adj_hi;          // boundary rows (compact), adjacent range
+  int32_t I0, nI;                      // internal separators (T positions), count
+  const int32_t *Bmap;                 // compact boundary index -> T position (nB)
+  const double *W;                     // nI x wb row-major, W = T_II^{-1} T_IB
+  const double *Wt;                    // wb x nI row-major
+  TriTiles LI, LB;                     // (T_II)^{-1} factor tiles, reduced L~^{-1} tiles
+  double *send, *recv, *tB, *yB, *zI, *zI2;   // nB, nB, nB, nB, nI, nI
 };
 
 }  // namespace strom
