@@ -1346,16 +1346,19 @@ strom_status device_partition_factors(strom_admm *h, SolverHandles &H, double *T
         (st = h->alloc(Z, (size_t)ni * wb)) || (st = h->alloc(W, (size_t)ni * wb)))
       return st;
     k_gather_sym<<<(unsigned)(((int64_t)ni * ni + 255) / 256), 256, 0, h->stream>>>(T, nS, dI, ni, dI, ni, A);
-    k_gather_sym<<<(unsigned)(((int64_t)ni * wb + 255) / 256), 256, 0, h->stream>>>(T, nS, dI, ni, dB + alo, wb, TIB);
+    if (wb > 0)
+      k_gather_sym<<<(unsigned)(((int64_t)ni * wb + 255) / 256), 256, 0, h->stream>>>(T, nS, dI, ni, dB + alo, wb, TIB);
     CK(cudaGetLastError());
     if ((st = chol_inverse(H, h->stream, ni, A, dinfo, "an internal separator block"))) return st;
     const double one = 1.0, mone = -1.0;
-    CBLAS(cublasDtrmm(H.blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, ni, wb,
-                      &one, A, ni, TIB, ni, Z, ni));                 // L^{-1} T_IB
-    CBLAS(cublasDtrmm(H.blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, ni, wb,
-                      &one, A, ni, Z, ni, W, ni));                   // W = L^{-T} L^{-1} T_IB
-    CBLAS(cublasDgemm(H.blas, CUBLAS_OP_T, CUBLAS_OP_N, wb, wb, ni, &mone, TIB, ni, W, ni, &one,
-                      Tt + (int64_t)alo * nB + alo, nB));           // T~[adj, adj] -= T_IB^T W
+    if (wb > 0) {
+      CBLAS(cublasDtrmm(H.blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, ni, wb,
+                        &one, A, ni, TIB, ni, Z, ni));               // L^{-1} T_IB
+      CBLAS(cublasDtrmm(H.blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, ni, wb,
+                        &one, A, ni, Z, ni, W, ni));                 // W = L^{-T} L^{-1} T_IB
+      CBLAS(cublasDgemm(H.blas, CUBLAS_OP_T, CUBLAS_OP_N, wb, wb, ni, &mone, TIB, ni, W, ni, &one,
+                        Tt + (int64_t)alo * nB + alo, nB));         // T~[adj, adj] -= T_IB^T W
+    }
     if (q == p.r) {
       if ((st = alloc_tiles(h, ni, A, h->pd.LI))) return st;
       h->pd.Wt = W;                                                  // column-major W == row-major W^T
@@ -1522,8 +1525,11 @@ static strom_status setup_impl(strom_admm **out, const strom_sdp *sdp_h, const s
   const int m = s.m;
   // ---- horizon partition -------------------------------------
   h->rank = rank; h->nranks = nranks;
-  h->part = nranks > 1;
-  h->xfer = nranks > 1 ? xfer : 0;
+  // STROM_FORCE_PARTITION=1 runs a single rank through the partitioned code path with a
+  // one-rank NCCL communicator (tests the allreduces captured in the graph on one GPU)
+  static const bool force = [] { const char *e = getenv("STROM_FORCE_PARTITION"); return e && e[0] == '1'; }();
+  h->part = nranks > 1 || (force && xfer == 1);
+  h->xfer = h->part ? xfer : 0;
   if ((st = make_plan(s, F, nranks, rank, h->plan))) return st;
   h->plans.resize(nranks);
   for (int q = 0; q < nranks; ++q)
@@ -1788,7 +1794,8 @@ static strom_status setup_impl(strom_admm **out, const strom_sdp *sdp_h, const s
   // ---- multi-GPU: NCCL communicator ------------------------------------------------
   if (h->xfer == 1) {
     ncclUniqueId id;
-    std::memcpy(&id, nccl_unique_id, sizeof(id));
+    if (nccl_unique_id) std::memcpy(&id, nccl_unique_id, sizeof(id));
+    else if (ncclGetUniqueId(&id) != ncclSuccess) { set_error("ncclGetUniqueId failed"); return STROM_ENCCL; }
     if (ncclCommInitRank(&h->comm, nranks, id, rank) != ncclSuccess) {
       set_error("ncclCommInitRank failed");
       return STROM_ENCCL;

@@ -537,3 +537,41 @@ def test_device_pointer_start_and_get():
         gb.get_device(Xo[:-1], None, None)
     with pytest.raises(ValueError):
         gb.set_start_device(Xd.cpu(), None, None)
+
+
+_FORCED = r"""
+import numpy as np, sys
+sys.path.insert(0, %r)
+import paper_2406_05846_b200 as S
+from oracle import Oracle
+from strom_inputs import compile_relaxation, models
+sdp = compile_relaxation(models.pendulum(5, 0.3, 1.0))
+g = S.StromAdmm(S.StromSdp(sdp), S.strom_admm_default_config(check_every=10))
+o = Oracle(sdp)
+g.iterate(30); o.iterate(30)
+X, y, Sg, r = g.get()
+rel = lambda a, b: np.linalg.norm(a - b) / max(1.0, np.linalg.norm(b))
+print("ERR", rel(X, o.X), rel(Sg, o.S), r["iter"])
+ok, it = g.solve(1e-4, 5000)
+o2 = Oracle(sdp); it2, ok2 = o2.solve_to_tol(1e-4, 5000)
+print("SOLVE", ok, it + 30, ok2, it2)
+"""
+
+
+def test_partition_path_with_nccl_allreduce_in_graph():
+    """The multi-GPU code path with its NCCL allreduces captured in the CUDA graph, run as
+    one rank (STROM_FORCE_PARTITION=1, a one-rank communicator; NCCL cannot put two ranks on
+    one GPU): 30 iterations match the oracle and solve() terminates on the device flag the
+    residual allreduce feeds."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, STROM_FORCE_PARTITION="1")
+    out = subprocess.run([sys.executable, "-c", _FORCED % root], env=env, capture_output=True, text=True,
+                         timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    err = [l for l in out.stdout.splitlines() if l.startswith("ERR")][0].split()
+    assert float(err[1]) <= 1e-9 and float(err[2]) <= 1e-9 and int(err[3]) == 30, err
+    sol = [l for l in out.stdout.splitlines() if l.startswith("SOLVE")][0].split()
+    assert sol[1] == "True" and sol[3] == "True", sol

@@ -1,5 +1,7 @@
 """A/B per-iteration time of two libstrom builds on pendulum N (alternating runs in
-separate processes).  python tools/ab_time.py LIB_A LIB_B [N] [reps]"""
+separate processes).  python tools/ab_time.py A B [N] [reps]; A and B are either built
+libstrom.so files (same binding) or checkout directories (each with its own binding and
+in-tree build, e.g. a git worktree of an older commit)."""
 import os
 import subprocess
 import sys
@@ -9,7 +11,7 @@ N = sys.argv[3] if len(sys.argv) > 3 else "30"
 reps = int(sys.argv[4]) if len(sys.argv) > 4 else 3
 code = r'''
 import os, sys, torch
-sys.path.insert(0, os.getcwd())
+sys.path.insert(0, os.environ.get("AB_ROOT", os.getcwd()))
 import paper_2406_05846_b200 as S
 from strom_inputs import compile_relaxation, models
 N = int(sys.argv[1])
@@ -28,7 +30,11 @@ print(f"{best:.3f}")
 res = {A: [], B: []}
 for r in range(reps):
     for lib in (A, B):
-        env = dict(os.environ, STROM_LIB=os.path.abspath(lib))
+        if os.path.isdir(lib):
+            env = dict(os.environ, AB_ROOT=os.path.abspath(lib))
+            env.pop("STROM_LIB", None)
+        else:
+            env = dict(os.environ, STROM_LIB=os.path.abspath(lib))
         out = subprocess.run([sys.executable, "-c", code, N], env=env, capture_output=True, text=True)
         try:
             res[lib].append(float(out.stdout.strip().splitlines()[-1]))
