@@ -191,6 +191,28 @@ strom_status strom_admm_lower_bound(strom_admm *h, const double *R_beta, double 
  * the solver state are unchanged. EINVAL on NULL handle/lam12. */
 strom_status strom_admm_extract(strom_admm *h, double *lam12, double *vtop);
 
+/* ---- batched instances (NEXT-2: the paper's grid of initial states) ----
+ * `count` single-GPU handles on one device, each with its own stream, iterated by ONE CUDA
+ * graph in which every handle's `iters_per_launch` iterations form an independent branch
+ * (a fork on `cuda_stream`, NULL = own stream, and a join), so the instances run
+ * concurrently and fill the SMs one instance leaves idle. Every handle keeps its own
+ * iterate, residuals, sigma and termination; results equal separate runs bitwise. The
+ * handles stay owned by the caller and must outlive the batch; strom_admm_get etc. on a
+ * handle are ordered after the batch's work. EINVAL on mixed devices, shared streams or
+ * partitioned (multi-GPU) handles. */
+typedef struct strom_batch strom_batch;
+strom_status strom_batch_create(strom_batch **out, strom_admm *const *handles, int32_t count,
+                                int32_t iters_per_launch, void *cuda_stream);
+void strom_batch_destroy(strom_batch *b);
+/* Exactly `iters` iterations of every instance (a multiple of iters_per_launch). Async. */
+strom_status strom_batch_iterate(strom_batch *b, int64_t iters);
+/* Iterates until every instance has eta <= tol (each stops at its own first such
+ * iteration) or maxiter; iters_done[count] (nullable) = iterations each instance performed,
+ * converged[count] (nullable) = 1 where eta <= tol was reached. OK when all converged,
+ * MAXITER otherwise, EDIVERGED on NaN/Inf in any instance. */
+strom_status strom_batch_solve(strom_batch *b, double tol, int64_t maxiter, int64_t *iters_done,
+                               int32_t *converged);
+
 /* Number of kernel launches one iteration issues (for launch accounting). */
 int32_t strom_admm_launches_per_iter(const strom_admm *h);
 /* Size of the factor data on the device in bytes, and unique dense factors. */

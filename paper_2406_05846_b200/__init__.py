@@ -33,6 +33,7 @@ EXPORTS = [
     "strom_debug_project_psd", "strom_debug_spmv", "strom_debug_solve", "strom_debug_host_solve",
     "strom_debug_eps", "strom_debug_link_virtual", "strom_debug_iterate_virtual",
     "strom_debug_host_part", "strom_debug_setup_virtual",
+    "strom_batch_create", "strom_batch_destroy", "strom_batch_iterate", "strom_batch_solve",
 ]
 
 
@@ -111,6 +112,10 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "strom_debug_solve": (I32, [VP, P(D), P(D)]),
         "strom_debug_host_solve": (I32, [VP, P(strom_admm_config), P(D), P(D)]),
         "strom_debug_eps": (D, [VP]),
+        "strom_batch_create": (I32, [P(VP), P(VP), I32, I32, VP]),
+        "strom_batch_destroy": (None, [VP]),
+        "strom_batch_iterate": (I32, [VP, I64]),
+        "strom_batch_solve": (I32, [VP, D, I64, P(I64), P(I32)]),
         "strom_debug_host_part": (I32, [VP, P(strom_admm_config), I32, I32, P(D), P(D), P(D), P(D), P(I32)]),
         "strom_debug_link_virtual": (I32, [P(VP), I32, VP]),
         "strom_debug_setup_virtual": (I32, [P(VP), VP, P(strom_admm_config), C.c_int, VP, C.c_int, C.c_int]),
@@ -414,6 +419,38 @@ class StromAdmm:
     def __del__(self):
         if getattr(self, "handle", None) and _lib is not None:
             _lib.strom_admm_destroy(self.handle)
+            self.handle = None
+
+
+class StromBatch:
+    """strom_batch_create: several StromAdmm handles (one device, own streams) iterated by
+    one CUDA graph with a concurrent branch per instance (NEXT-2)."""
+
+    def __init__(self, admms, iters_per_launch: int = 50, stream=None):
+        lib = load()
+        self.admms = list(admms)            # the handles must outlive the batch
+        arr = (C.c_void_p * len(self.admms))(*[a.handle.value for a in self.admms])
+        h = C.c_void_p()
+        _check(lib.strom_batch_create(C.byref(h), arr, len(self.admms), int(iters_per_launch),
+                                      _torch_stream_ptr(stream)), "strom_batch_create")
+        self.handle, self.K = h, int(iters_per_launch)
+
+    def iterate(self, iters: int):
+        return _check(load().strom_batch_iterate(self.handle, int(iters)), "strom_batch_iterate")
+
+    def solve(self, tol: float, maxiter: int):
+        """-> (all converged, iterations per instance, converged flags per instance)"""
+        B = len(self.admms)
+        done = np.zeros(B, dtype=np.int64)
+        conv = np.zeros(B, dtype=np.int32)
+        st = _check(load().strom_batch_solve(self.handle, float(tol), int(maxiter),
+                                             done.ctypes.data_as(C.POINTER(C.c_int64)),
+                                             conv.ctypes.data_as(C.POINTER(C.c_int32))), "strom_batch_solve")
+        return st == STROM_OK, done, conv.astype(bool)
+
+    def __del__(self):
+        if getattr(self, "handle", None) and _lib is not None:
+            _lib.strom_batch_destroy(self.handle)
             self.handle = None
 
 

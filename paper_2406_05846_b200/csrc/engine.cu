@@ -2068,6 +2068,162 @@ strom_status strom_nccl_get_unique_id(void *id128) {
   return STROM_OK;
 }
 
+// ---- batched instances (NEXT-2) ---------------------------------------
+// B independent handles (e.g. the paper's grid of pendulum initial states) in
+// ONE CUDA graph: a fork on the batch stream, every handle's K iterations captured on its own
+// streams (independent branches), a join. The GPU runs the branches concurrently -- one
+// instance's 30 moment-block CTAs occupy 30 of 148 SMs -- and every handle keeps its own
+// state, residuals, sigma and done flag (a finished instance's kernels are no-ops).
+}  // extern "C"
+struct strom_batch {
+  std::vector<strom_admm *> hs;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int K = 1;
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t ex = nullptr;
+  cudaEvent_t fork = nullptr, done_ev = nullptr;
+  std::vector<cudaEvent_t> joins, pre;
+  DevState *hstate = nullptr;            // pinned host copies of every handle's DevState
+  ~strom_batch() {
+    if (ex) cudaGraphExecDestroy(ex);
+    if (g) cudaGraphDestroy(g);
+    if (fork) cudaEventDestroy(fork);
+    if (done_ev) cudaEventDestroy(done_ev);
+    for (cudaEvent_t e : joins) cudaEventDestroy(e);
+    for (cudaEvent_t e : pre) cudaEventDestroy(e);
+    if (hstate) cudaFreeHost(hstate);
+    if (own_stream && stream) cudaStreamDestroy(stream);
+  }
+};
+extern "C" {
+
+strom_status strom_batch_create(strom_batch **out, strom_admm *const *handles, int32_t count,
+                                int32_t iters_per_launch, void *cuda_stream) {
+  if (!out || !handles || count < 1 || iters_per_launch < 1) {
+    set_error("strom_batch_create: bad arguments");
+    return STROM_EINVAL;
+  }
+  *out = nullptr;
+  std::unique_ptr<strom_batch> b(new strom_batch);
+  for (int i = 0; i < count; ++i) {
+    strom_admm *h = handles[i];
+    if (!h || h->device != handles[0]->device || h->xfer != 0) {
+      set_error("strom_batch_create: handles must be single-GPU handles on one device");
+      return STROM_EINVAL;
+    }
+    for (int j = 0; j < i; ++j)
+      if (handles[j] == h || handles[j]->stream == h->stream) {
+        set_error("strom_batch_create: every handle needs its own stream");
+        return STROM_EINVAL;
+      }
+    b->hs.push_back(h);
+  }
+  CK(cudaSetDevice(handles[0]->device));
+  b->K = iters_per_launch;
+  if (cuda_stream) b->stream = (cudaStream_t)cuda_stream;
+  else { CK(cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking)); b->own_stream = true; }
+  CK(cudaEventCreateWithFlags(&b->fork, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&b->done_ev, cudaEventDisableTiming));
+  b->joins.resize(count);
+  b->pre.resize(count);
+  for (auto &e : b->joins) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  for (auto &e : b->pre) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  CK(cudaMallocHost(&b->hstate, sizeof(DevState) * count));
+  for (strom_admm *h : b->hs) CK(cudaStreamSynchronize(h->stream));
+  CK(cudaStreamBeginCapture(b->stream, cudaStreamCaptureModeThreadLocal));
+  strom_status st = STROM_OK;
+  cudaError_t e = cudaEventRecord(b->fork, b->stream);
+  for (int i = 0; i < count && st == STROM_OK && e == cudaSuccess; ++i) {
+    strom_admm *h = b->hs[i];
+    e = cudaStreamWaitEvent(h->stream, b->fork, 0);
+    for (int k = 0; k < b->K && st == STROM_OK && e == cudaSuccess; ++k) {
+      int nl = 0;
+      st = launch_iteration(h, nl);
+    }
+    if (e == cudaSuccess) e = cudaEventRecord(b->joins[i], h->stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(b->stream, b->joins[i], 0);
+  }
+  cudaGraph_t graph = nullptr;
+  cudaError_t e2 = cudaStreamEndCapture(b->stream, &graph);
+  if (st != STROM_OK || e != cudaSuccess || e2 != cudaSuccess) {
+    if (graph) cudaGraphDestroy(graph);
+    if (st == STROM_OK) { set_error(std::string("strom_batch_create: capture: ") + cudaGetErrorString(e != cudaSuccess ? e : e2)); st = STROM_ECUDA; }
+    return st;
+  }
+  b->g = graph;
+  CK(cudaGraphInstantiate(&b->ex, b->g, 0));
+  *out = b.release();
+  return STROM_OK;
+}
+
+void strom_batch_destroy(strom_batch *b) { delete b; }
+
+static strom_status batch_start(strom_batch *b) {
+  // the batch stream is ordered after work queued on the handles' own streams (set_start...)
+  for (size_t i = 0; i < b->hs.size(); ++i) {
+    CK(cudaEventRecord(b->pre[i], b->hs[i]->stream));
+    CK(cudaStreamWaitEvent(b->stream, b->pre[i], 0));
+  }
+  return STROM_OK;
+}
+
+static strom_status batch_finish(strom_batch *b) {
+  // the handles' own streams (get(), set_start()) are ordered after the batch's work
+  CK(cudaEventRecord(b->done_ev, b->stream));
+  for (strom_admm *h : b->hs) CK(cudaStreamWaitEvent(h->stream, b->done_ev, 0));
+  return STROM_OK;
+}
+
+strom_status strom_batch_iterate(strom_batch *b, int64_t iters) {
+  strom_status st_;
+  if (!b || iters < 0 || iters % b->K != 0) {
+    set_error("strom_batch_iterate: iters must be a non-negative multiple of iters_per_launch");
+    return STROM_EINVAL;
+  }
+  CK(cudaSetDevice(b->hs[0]->device));
+  if ((st_ = batch_start(b))) return st_;
+  for (strom_admm *h : b->hs) k_set_control<<<1, 1, 0, b->stream>>>(h->st, -1.0);
+  CK(cudaGetLastError());
+  for (int64_t left = iters; left > 0; left -= b->K) CK(cudaGraphLaunch(b->ex, b->stream));
+  return batch_finish(b);
+}
+
+strom_status strom_batch_solve(strom_batch *b, double tol, int64_t maxiter, int64_t *iters_done,
+                               int32_t *converged) {
+  if (!b || maxiter < 0 || !(tol >= 0.0)) { set_error("strom_batch_solve: bad arguments"); return STROM_EINVAL; }
+  CK(cudaSetDevice(b->hs[0]->device));
+  const int B = (int)b->hs.size();
+  strom_status st0 = batch_start(b);
+  if (st0) return st0;
+  std::vector<int64_t> it0(B);
+  for (int i = 0; i < B; ++i) {
+    CK(cudaMemcpyAsync(&b->hstate[i], b->hs[i]->st, sizeof(DevState), cudaMemcpyDeviceToHost, b->stream));
+    k_set_control<<<1, 1, 0, b->stream>>>(b->hs[i]->st, tol);
+  }
+  CK(cudaStreamSynchronize(b->stream));
+  for (int i = 0; i < B; ++i) it0[i] = b->hstate[i].iter;
+  bool all = false;
+  for (int64_t left = maxiter; left > 0 && !all; left -= b->K) {
+    CK(cudaGraphLaunch(b->ex, b->stream));
+    for (int i = 0; i < B; ++i)
+      CK(cudaMemcpyAsync(&b->hstate[i], b->hs[i]->st, sizeof(DevState), cudaMemcpyDeviceToHost, b->stream));
+    CK(cudaStreamSynchronize(b->stream));
+    all = true;
+    for (int i = 0; i < B; ++i) all = all && b->hstate[i].done;
+  }
+  bool nan = false;
+  for (int i = 0; i < B; ++i) {
+    if (iters_done) iters_done[i] = b->hstate[i].iter - it0[i];
+    if (converged) converged[i] = b->hstate[i].done && !b->hstate[i].nan_flag;
+    nan = nan || b->hstate[i].nan_flag;
+  }
+  strom_status st = batch_finish(b);
+  if (st) return st;
+  if (nan) { set_error("strom_batch_solve: NaN/Inf in an instance"); return STROM_EDIVERGED; }
+  return all ? STROM_OK : STROM_MAXITER;
+}
+
 // ---- in-process virtual ranks (test harness for the multi-GPU path) ------------------
 // nranks handles made by strom_debug_setup_virtual (rank r of nranks, one device) play the
 // NCCL ranks: the same segments are launched, and each sum over ranks is a kernel that adds

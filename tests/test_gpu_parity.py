@@ -575,3 +575,32 @@ def test_partition_path_with_nccl_allreduce_in_graph():
     assert float(err[1]) <= 1e-9 and float(err[2]) <= 1e-9 and int(err[3]) == 30, err
     sol = [l for l in out.stdout.splitlines() if l.startswith("SOLVE")][0].split()
     assert sol[1] == "True" and sol[3] == "True", sol
+
+
+def test_batched_instances_match_separate_runs():
+    """NEXT-2: a batch of grid instances in one graph with a branch per
+    instance gives bitwise the iterates of separate runs, and batch solve stops every
+    instance at its own first iteration with eta <= tol (the separate solve's count)."""
+    states = [(0.3, 1.0), (1.2, -3.0), (2.0, 0.5)]
+    sdps = [compile_relaxation(models.pendulum(5, *st)) for st in states]
+    sep = [make(sdp, check_every=10) for sdp in sdps]
+    for g in sep:
+        g.iterate(40)
+    bat = [S.StromAdmm(S.StromSdp(sdp), S.strom_admm_default_config(check_every=10),
+                       stream=torch.cuda.Stream()) for sdp in sdps]
+    B = S.StromBatch(bat, iters_per_launch=10)
+    B.iterate(40)
+    for g, h in zip(sep, bat):
+        a, b = g.get(), h.get()
+        for k in range(3):
+            assert np.array_equal(a[k], b[k])
+        assert a[3]["iter"] == b[3]["iter"] == 40
+    # solve to tolerance from a fresh start
+    sep2 = [make(sdp, check_every=10) for sdp in sdps]
+    its = [g.solve(1e-5, 20000)[1] for g in sep2]
+    for h in bat:
+        h.set_start()
+    ok, done, conv = B.solve(1e-5, 20000)
+    assert ok and conv.all() and list(done) == its, (list(done), its)
+    for g, h in zip(sep2, bat):
+        assert np.array_equal(g.get()[0], h.get()[0])
