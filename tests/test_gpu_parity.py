@@ -261,14 +261,16 @@ def test_large_block_iterations_parity(name):
     _compare(g, o, 1e-9, f"{name}@20")
 
 
-@pytest.mark.parametrize("shape,N", [("carback", 30), ("flying", 60), ("cartpole", 30)])
+@pytest.mark.parametrize("shape,N", [("flying", 60), ("landing", 50)])
 def test_full_size_properties(shape, N):
-    """BASELINE configs[2..4] at full size in the bench's launch configuration, checked by
-    properties that hold at any size (the oracle is too slow here):
+    """The paper's largest configs (BASELINE configs[3]: flying robot N=60, n = 1.73M;
+    landing N=50) at full size in the bench's launch configuration, checked by properties
+    that hold at any size (their oracle parity runs at N = 6 below):
       F3: A(X^{k+1}) - b = (1 - tau)(A(X^k) - b) - tau sigma eps y^{k+1}
       S^{k+1} in Omega_+ (sampled blocks) and eta recomputed on the host from (X, y, S)."""
     import scipy.sparse as sp
-    sdp = compile_relaxation(models.synthetic_shape(shape, N, seed=0))
+    from strom_inputs.paper_models import paper_instance
+    sdp = compile_relaxation(paper_instance(shape, N))
     g = make(sdp, check_every=10)
     A = sp.csr_matrix((sdp.A_data, sdp.A_indices, sdp.A_indptr), shape=(sdp.m, sdp.n))
     g.iterate(4)
@@ -310,7 +312,8 @@ def test_horizon_partition_virtual_ranks(name, P):
     iterate equals the single-GPU run to rounding (the partitioned separator solve
     reassociates: <= 1e-12 relative), every rank holds the same iterate and takes the same
     eta / termination decisions, and the result matches the oracle."""
-    sdp = (compile_relaxation(models.synthetic_shape("carback", 8, seed=5)) if name == "carback8" else case(name))
+    from strom_inputs.paper_models import paper_instance
+    sdp = (compile_relaxation(paper_instance("carback", 8, seed=5)) if name == "carback8" else case(name))
     ref = make(sdp, check_every=5)
     hs, ranks = _virtual_ranks(sdp, P, check_every=5)
     ref.iterate(12)
@@ -498,11 +501,13 @@ def test_final_objective_and_certificate_parity(name, state, policy):
 @pytest.mark.parametrize("shape,N,iters", [("cartpole", 30, 10), ("carback", 30, 6), ("flying", 6, 10),
                                            ("landing", 6, 10)])
 def test_full_size_large_shapes_oracle_parity(shape, N, iters):
-    """BASELINE configs[2..4] shapes against the oracle element by element: cart-pole at its
-    full size (n = 195,300, 105/14 blocks), car back-in at its full size (n = 669,750,
-    190/19 blocks: the 2-CTA cluster K-EIG and 29 separators), flying robot (231/21) and
-    landing (190/19, 495-row separators) at N = 6, in the bench's launch configuration."""
-    sdp = compile_relaxation(models.synthetic_shape(shape, N, seed=0))
+    """The paper's models (App. E; BASELINE configs[2..4]) against the oracle element by
+    element: cart-pole at its full size (n = 176,400, 105/14 blocks), car back-in at its
+    full size (n = 658,350, 190/19 blocks: the 2-CTA cluster K-EIG and 29 separators),
+    flying robot (231/21) and landing (190/19, 495-row separators) at N = 6, in the bench's
+    launch configuration."""
+    from strom_inputs.paper_models import paper_instance
+    sdp = compile_relaxation(paper_instance(shape, N, seed=1))
     g = make(sdp, check_every=iters)
     o = Oracle(sdp)
     g.iterate(1); o.iterate(1)
