@@ -791,6 +791,12 @@ constexpr int kClusterEig = 2;
 
 __host__ __device__ inline int eig_cluster_rows(int n) { return (n + kClusterEig - 1) / kClusterEig; }
 inline bool eig_use_cluster(int n) { return n > 112 && n <= 236; }
+// cluster size of the large-block K-EIG: 4 (k_eig_cl, default) or 2 (k_eig_cluster);
+// STROM_EIG_CL=2 selects the 2-CTA kernel
+inline int eig_cl_size() {
+  static const int c = [] { const char *e = getenv("STROM_EIG_CL"); return e && atoi(e) == 2 ? 2 : 4; }();
+  return c;
+}
 inline size_t eig_cluster_smem_bytes(int n) {
   const int NP = n + (n & 1), H = NP / 2, h = eig_cluster_rows(n);
   return sizeof(double) * ((size_t)h * n + n /*norms*/ + n /*lambda*/ + 2 * (size_t)H /*partials*/ + 16);
@@ -1019,6 +1025,260 @@ __global__ void __cluster_dims__(kClusterEig, 1, 1) __launch_bounds__(512, 1) k_
     while (j * (j + 1) / 2 > e) --j;
     while ((j + 1) * (j + 2) / 2 <= e) ++j;
     const int i = e - j * (j + 1) / 2;
+    double acc = 0.0;
+    for (int c = 0; c < cnt; ++c) {
+      const int k = sets[c];
+      acc += lam[k] * Vg[k * n + i] * Vg[k * n + j];
+    }
+    double sv;
+    if (use_pos) {
+      const double xb = Xb[e];
+      sv = (acc - (i == j ? xb : xb * isq2)) * is;
+    } else {
+      sv = -acc * is;
+    }
+    a.S_out[off + e] = (i == j) ? sv : sv * 1.41421356237309504880;
+  }
+}
+
+// ============================================================================
+// K-EIG, CL-CTA cluster variant with register-resident pairs (orders 113..236; car
+// back-in / landing 190, flying robot 231). CTA r of the cluster holds
+// rows [r h, r h + h) of U = (X_b + sI) V (h = ceil(n / CL)). One round: G lanes own a
+// column pair for ALL pairs at once (CL = 4: 48-58 local rows, G = 4 -> 128 pairs per
+// pass >= n/2), load its local rows into registers, form the partial dot, publish it; one
+// cluster barrier; every CTA sums the CL partials in rank order (identical rotations in
+// all CTAs), rotates the registers and stores them back; one CTA barrier. U is read and
+// written once per round (the 2-CTA kernel above reads it twice and runs 3 passes).
+// ============================================================================
+__host__ __device__ inline int eig_cl_rows(int n, int CL) { return (n + CL - 1) / CL; }
+// column stride (doubles) of the local rows: >= h and == 4 (mod 16), so the 4-double row
+// segments that the 8 lane groups of a warp read from (mostly consecutive) columns start
+// at banks 0, 8, 16, 24 in turn: two wavefronts per load instead of eight (h = 48)
+__host__ __device__ inline int eig_cl_ld(int h) { return (h + 11) / 16 * 16 + 4; }
+inline size_t eig_cl_smem_bytes(int n, int CL) {
+  const int NP = n + (n & 1), H = NP / 2, ld = eig_cl_ld(eig_cl_rows(n, CL));
+  return sizeof(double) * ((size_t)ld * n + n /*norms*/ + n /*lambda*/ + 2 * (size_t)H /*partials*/ + 16);
+}
+
+template <int CL, int G, int EPL>
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(512, 1) k_eig_cl(EigArgs a) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  if (a.st->done) return;                     // uniform across the cluster
+  extern __shared__ double sm[];
+  __shared__ double red[4 * 32];
+  __shared__ int sets[128];
+  __shared__ int set_info;
+  constexpr int PPW = 32 / G;
+  const int crank = (int)cl.block_rank();
+  const int bidx = a.blocks[blockIdx.x / CL];
+  const int n = a.bn[bidx];
+  const int NP = n + (n & 1), H = NP / 2;
+  const int h = eig_cl_rows(n, CL);
+  const int r0 = crank * h, nloc = max(0, min(h, n - r0));   // local rows [r0, r0 + nloc)
+  const int64_t off = a.boff[bidx];
+  const int L = n * (n + 1) / 2;
+  const int ldc = eig_cl_ld(h);
+  double *U = sm;                                   // column j, local row i: U[j*ldc + i]
+  double *nrm = sm + (size_t)ldc * n;               // n
+  double *lamv = nrm + n;                           // n
+  double *part = lamv + n;                          // 2 x H (parity)
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5, nwarps = nt >> 5;
+  const int grp = lane / G, sub = lane % G;
+  const double sigma = a.st->sigma;
+  const double isq2 = 0.70710678118654752440;
+  const bool proj = (a.mode == 0);
+  // ---- 1. gather X_b (each CTA 1/CL of the svec entries), Frobenius norm ---------------
+  double fro = gather_xb(a, off, L, crank * nt + tid, CL * nt, sigma, proj);
+  {
+    double v1[1] = {fro};
+    block_sum<1>(v1, red);
+    if (tid == 0) part[0] = v1[0];
+  }
+  cl.sync();                                        // Xb_out and every partial norm visible
+  double s;
+  {
+    double tot = 0.0;
+    for (int c = 0; c < CL; ++c) tot += cl.map_shared_rank(part, c)[0];
+    s = 2.0 * sqrt(tot) + 1e-300;
+  }
+  cl.sync();                                        // partial slot reused below
+  const double *Xb = a.Xb_out + off;
+  // ---- 2. local rows of U = (X_b + sI) V, V = V_prev (warm) or I ------------------------
+  const bool warm = proj && a.warm_enable && a.st->eig_warm_valid &&
+                    (a.cold_every <= 0 || (a.st->iter % a.cold_every) != 0);
+  if (warm) {
+    const double *Vp = a.Vstore + a.voff[bidx];
+    for (int e = tid; e < nloc * n; e += nt) {
+      const int j = e / nloc, il = e - j * nloc, i = r0 + il;
+      const double *vj = Vp + (int64_t)j * n;
+      double t0 = 0.0, t1 = 0.0;
+      int k = 0;
+      for (; k + 1 < n; k += 2) {
+        const double a0 = Xb[svec_pos(i, k)], a1 = Xb[svec_pos(i, k + 1)];
+        t0 += (i == k ? a0 : a0 * isq2) * vj[k];
+        t1 += (i == k + 1 ? a1 : a1 * isq2) * vj[k + 1];
+      }
+      if (k < n) { const double a0 = Xb[svec_pos(i, k)]; t0 += (i == k ? a0 : a0 * isq2) * vj[k]; }
+      U[j * ldc + il] = (t0 + t1) + s * vj[i];
+    }
+  } else {
+    for (int e = tid; e < nloc * n; e += nt) {
+      const int j = e / nloc, il = e - j * nloc, i = r0 + il;
+      const double v = Xb[svec_pos(i, j)];
+      U[j * ldc + il] = (i == j) ? v + s : v * isq2;
+    }
+  }
+  __syncthreads();
+  cl.sync();          // every CTA has read V_prev before anyone overwrites it (step 4)
+  // ---- 3. sweeps --------------------------------------------------------------------------
+  const double tol = fmax(a.tol, 4.0 * n * 2.220446049250313e-16);
+  const double tol2 = tol * tol, quad2 = 1e-18;
+  bool converged = false;
+  int sweep = 0;
+  const int P = warp * PPW + grp;                   // this lane group's pair slot (one pass)
+  for (; sweep < a.max_sweeps; ++sweep) {
+    for (int j = warp; j < n; j += nwarps) {        // exact column norms (DSMEM sum)
+      const double *uj = U + j * ldc;
+      double t = 0.0;
+      for (int i = lane; i < nloc; i += 32) t += uj[i] * uj[i];
+      t = warp_sum(t);
+      if (lane == 0) lamv[j] = t;
+    }
+    cl.sync();
+    for (int j = tid; j < n; j += nt) {
+      double t = 0.0;
+      for (int c = 0; c < CL; ++c) t += cl.map_shared_rank(lamv, c)[j];
+      nrm[j] = t;
+    }
+    cl.sync();                                      // lamv free again; nrm complete
+    int rotated = 0, big = 0;
+    for (int r = 0; r < NP - 1; ++r) {
+      double *pr = part + (r & 1) * H;
+      int p = 0, q = 0;
+      bool valid = P < H;
+      if (valid) {
+        p = rr_pos(P, r, NP - 1); q = rr_pos(NP - 1 - P, r, NP - 1);
+        if (p > q) { const int t2 = p; p = q; q = t2; }
+        valid = q < n;
+      }
+      double xp[EPL], xq[EPL];
+      double g0 = 0.0, g1 = 0.0;
+      double *up = U + p * ldc, *uq = U + q * ldc;
+#pragma unroll
+      for (int c = 0; c < EPL; ++c) {
+        const int i = sub + G * c;
+        const bool ok = valid && i < nloc;
+        xp[c] = ok ? up[i] : 0.0;
+        xq[c] = ok ? uq[i] : 0.0;
+        if (c & 1) g1 += xp[c] * xq[c]; else g0 += xp[c] * xq[c];
+      }
+      const double gl = group_sum<G>(g0 + g1);
+      if (valid && sub == 0) pr[P] = gl;
+      cl.sync();                                    // every CTA's partial dot visible
+      if (valid) {
+        double ga = 0.0;
+        for (int c = 0; c < CL; ++c) ga += cl.map_shared_rank(pr, c)[P];
+        const double al = nrm[p], be = nrm[q];
+        const double ab = al * be, g2a = ga * ga;
+        if (ga != 0.0 && g2a > tol2 * ab) {
+          rotated = 1;
+          if (g2a > quad2 * ab) big = 1;
+          double cs, sn;
+          jacobi_cs(al, be, ga, cs, sn);
+#pragma unroll
+          for (int c = 0; c < EPL; ++c) {
+            const int i = sub + G * c;
+            if (i < nloc) { up[i] = cs * xp[c] - sn * xq[c]; uq[i] = sn * xp[c] + cs * xq[c]; }
+          }
+          if (sub == 0) {
+            const double c2 = cs * cs, s2 = sn * sn, csn = 2.0 * cs * sn * ga;
+            nrm[p] = c2 * al - csn + s2 * be;
+            nrm[q] = s2 * al + csn + c2 * be;
+          }
+        }
+      }
+      __syncthreads();                              // rotated columns visible to the next round
+    }
+    const int any_big = __syncthreads_or(big);
+    const int any_rot = __syncthreads_or(rotated);
+    if (!any_rot || !any_big) { converged = true; break; }
+  }
+  if (tid == 0 && crank == 0) {
+    if (!converged) atomicCAS(&a.st->eig_fail, 0, bidx + 1);
+    atomicAdd(&a.st->eig_sweeps, (unsigned long long)(sweep + 1));
+  }
+  // ---- 4. eigenpairs: exact norms (DSMEM), lambda = ||u|| - s, V = normalised U --------
+  for (int j = warp; j < n; j += nwarps) {
+    const double *uj = U + j * ldc;
+    double t = 0.0;
+    for (int i = lane; i < nloc; i += 32) t += uj[i] * uj[i];
+    t = warp_sum(t);
+    if (lane == 0) lamv[j] = t;
+  }
+  cl.sync();
+  for (int j = tid; j < n; j += nt) {
+    double t = 0.0;
+    for (int c = 0; c < CL; ++c) t += cl.map_shared_rank(lamv, c)[j];
+    nrm[j] = sqrt(t);                               // ||u_j||
+  }
+  cl.sync();
+  for (int j = tid; j < n; j += nt) lamv[j] = nrm[j] - s;
+  __syncthreads();
+  const double *lam = lamv;
+  if (a.mode == 2) {
+    double l1, l2;
+    const int j = top2(lam, n, l1, l2);
+    if (tid == 0 && crank == 0) { a.lam12[2 * bidx] = l1; a.lam12[2 * bidx + 1] = l2; }
+    const double v0 = cl.map_shared_rank(U, 0)[j * ldc];     // row 0 lives in CTA 0
+    const double sg = v0 < 0.0 ? -1.0 / nrm[j] : 1.0 / nrm[j];
+    for (int il = tid; il < nloc; il += nt) a.vtop[a.toff[bidx] + r0 + il] = U[j * ldc + il] * sg;
+    cl.sync();                                      // CTA 0's shared memory read by the others
+    return;
+  }
+  if (!proj) {
+    if (tid == 0 && crank == 0) {   // with the same error margin as k_eig
+      double lm = lam[0];
+      for (int k = 1; k < n; ++k) lm = fmin(lm, lam[k]);
+      a.lam_min[bidx] = lm - 1.5 * n * 2.220446049250313e-16 * s;
+    }
+    return;
+  }
+  // normalised local rows -> global V (column-major n x n) for the reconstruction
+  double *Vg = a.Vstore + a.voff[bidx];
+  for (int e = tid; e < nloc * n; e += nt) {
+    const int j = e / nloc, il = e - j * nloc;
+    Vg[j * n + r0 + il] = U[j * ldc + il] / nrm[j];
+  }
+  if (warp == 0) {                // the smaller eigen-set, ascending order, by ballots
+    int npos = 0, nneg = 0;
+    for (int k0 = 0; k0 < n; k0 += 32) {
+      const int k = k0 + lane;
+      const double l = k < n ? lam[k] : 0.0;
+      npos += __popc(__ballot_sync(0xffffffffu, l > 0.0));
+      nneg += __popc(__ballot_sync(0xffffffffu, l < 0.0));
+    }
+    const int use_pos = npos <= nneg;
+    int cnt = 0;
+    for (int k0 = 0; k0 < n; k0 += 32) {
+      const int k = k0 + lane;
+      const double l = k < n ? lam[k] : 0.0;
+      const bool pick = use_pos ? (l > 0.0) : (l < 0.0);
+      const unsigned b = __ballot_sync(0xffffffffu, pick);
+      if (pick) sets[cnt + __popc(b & ((1u << lane) - 1u))] = k;
+      cnt += __popc(b);
+    }
+    if (lane == 0) set_info = cnt * 2 + use_pos;
+  }
+  __threadfence();
+  cl.sync();                                        // V rows of every CTA visible in global
+  const int cnt = set_info >> 1, use_pos = set_info & 1;
+  const double is = 1.0 / sigma;
+  for (int e = crank * nt + tid; e < L; e += CL * nt) {
+    int i, j;
+    svec_ij(e, i, j);
     double acc = 0.0;
     for (int c = 0; c < cnt; ++c) {
       const int k = sets[c];

@@ -980,11 +980,16 @@ strom_status launch_eig(strom_admm *h, int mode, const double *yv, int &nl) {
     a.Ug = h->Ug; a.Ag = h->Ag; a.uoff = h->uoff;
     const int G = eig_G(np);
     if (eig_use_cluster(h->eig_class_n[c])) {
-      // 16 lanes per pair (three passes per round phase at order 190). 8 lanes (two passes,
-      // 15 rows per lane; STROM_EIG_CL8=1) measured slower: car back-in K-EIG 4.02 -> 4.59 ms.
-      static const bool cl8 = [] { const char *e = getenv("STROM_EIG_CL8"); return e && e[0] == '1'; }();
-      if (cl8) k_eig_cluster<8, 15><<<a.nblk * kClusterEig, 512, eig_cluster_smem_bytes(h->eig_class_n[c]), s>>>(a);
-      else k_eig_cluster<16, 8><<<a.nblk * kClusterEig, 512, eig_cluster_smem_bytes(h->eig_class_n[c]), s>>>(a);
+      const int nmax = h->eig_class_n[c];
+      if (eig_cl_size() == 4) {
+        // 4-CTA clusters, register-resident pairs, one pass per round (eig.cuh k_eig_cl)
+        const size_t sm4 = eig_cl_smem_bytes(nmax, 4);
+        if (nmax <= 192) k_eig_cl<4, 4, 12><<<a.nblk * 4, 512, sm4, s>>>(a);
+        else k_eig_cl<4, 4, 15><<<a.nblk * 4, 512, sm4, s>>>(a);
+      } else {
+        // 2-CTA clusters, 16 lanes per pair (three passes per round phase at order 190)
+        k_eig_cluster<16, 8><<<a.nblk * kClusterEig, 512, eig_cluster_smem_bytes(nmax), s>>>(a);
+      }
     } else if (eig_global(np)) k_eig<32, 8, true><<<a.nblk, threads, smem, s>>>(a);
     else if (G == 4) k_eig<4, 4, false><<<a.nblk, threads, smem, s>>>(a);
     else if (G == 8 && h->eig_class_n[c] <= 56)
@@ -1734,8 +1739,10 @@ static strom_status setup_impl(strom_admm **out, const strom_sdp *sdp_h, const s
       {
         CK(cudaFuncSetAttribute(k_eig_cluster<16, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)eig_cluster_smem_bytes(mx)));
-        CK(cudaFuncSetAttribute(k_eig_cluster<8, 15>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)eig_cluster_smem_bytes(mx)));
+        CK(cudaFuncSetAttribute(k_eig_cl<4, 4, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)eig_cl_smem_bytes(mx, 4)));
+        CK(cudaFuncSetAttribute(k_eig_cl<4, 4, 15>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)eig_cl_smem_bytes(mx, 4)));
       }
     }
     double best = -1.0;
