@@ -135,6 +135,11 @@ strom_status strom_admm_setup(strom_admm **out, const strom_sdp *sdp, const stro
                               int rank, int nranks);
 void strom_admm_destroy(strom_admm *h);
 
+/* New sigma, tau, sigma policy and eigensolver settings for a set-up handle (eps and
+ * check_every stay: the factor and the captured graphs depend on them). Takes effect at
+ * the next strom_admm_set_start. EINVAL on an invalid sigma / tau. */
+strom_status strom_admm_reconfigure(strom_admm *h, const strom_admm_config *cfg);
+
 /* Warm start (Algorithm 1 input X^0, S^0). Host buffers of full
  * length (X_svec[n], y[m], S_svec[n]); NULL means zeros. Resets the iteration
  * counter and sigma to cfg.sigma. */
@@ -161,6 +166,8 @@ typedef struct {
   double sigma;                 /* sigma that produced this iterate         */
   double eta_x;                 /* ||X - Pi(X_b)|| / (1 + ||X||), diagnostic */
   int64_t eig_sweeps;           /* Jacobi sweeps summed over blocks since setup */
+  int64_t iter_eta[3];          /* first iteration (since set_start) with eta <= 1e-4,
+                                   1e-5, 1e-6, tracked on the device; 0 = not reached */
 } strom_residuals;
 
 /* Copies the iterate to host buffers (NULL = skip). Synchronises the stream. */

@@ -34,6 +34,7 @@ EXPORTS = [
     "strom_debug_eps", "strom_debug_link_virtual", "strom_debug_iterate_virtual",
     "strom_debug_host_part", "strom_debug_setup_virtual",
     "strom_batch_create", "strom_batch_destroy", "strom_batch_iterate", "strom_batch_solve",
+    "strom_admm_reconfigure",
 ]
 
 
@@ -61,10 +62,14 @@ class strom_admm_config(C.Structure):
 class strom_residuals(C.Structure):
     _fields_ = [("iter", C.c_int64), ("eta_p", C.c_double), ("eta_d", C.c_double),
                 ("eta_g", C.c_double), ("pobj", C.c_double), ("dobj", C.c_double),
-                ("sigma", C.c_double), ("eta_x", C.c_double), ("eig_sweeps", C.c_int64)]
+                ("sigma", C.c_double), ("eta_x", C.c_double), ("eig_sweeps", C.c_int64),
+                ("iter_eta", C.c_int64 * 3)]
 
     def as_dict(self):
-        return {k: getattr(self, k) for k, _ in self._fields_}
+        d = {k: getattr(self, k) for k, _ in self._fields_}
+        d["iter_eta"] = {"1e-4": self.iter_eta[0] or None, "1e-5": self.iter_eta[1] or None,
+                         "1e-6": self.iter_eta[2] or None}
+        return d
 
 
 _lib: Optional[C.CDLL] = None
@@ -94,6 +99,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "strom_admm_setup": (I32, [P(VP), VP, P(strom_admm_config), C.c_int, VP, VP, C.c_int, C.c_int]),
         "strom_admm_destroy": (None, [VP]),
         "strom_admm_set_start": (I32, [VP, P(D), P(D), P(D)]),
+        "strom_admm_reconfigure": (I32, [VP, P(strom_admm_config)]),
         "strom_admm_set_start_device": (I32, [VP, VP, VP, VP]),
         "strom_admm_iterate": (I32, [VP, I64]),
         "strom_admm_solve": (I32, [VP, D, I64, P(I64)]),
@@ -310,6 +316,13 @@ class StromAdmm:
             cur.wait_stream(self.stream)
         else:
             torch.cuda.synchronize(self.device)
+
+    def reconfigure(self, **over):
+        """strom_admm_reconfigure: new sigma / tau / sigma policy / eigensolver settings,
+        effective at the next set_start."""
+        for k, v in over.items():
+            setattr(self.cfg, k, v)
+        return _check(load().strom_admm_reconfigure(self.handle, C.byref(self.cfg)), "strom_admm_reconfigure")
 
     def set_start(self, X=None, y=None, S=None):
         f = lambda a: None if a is None else np.ascontiguousarray(a, dtype=np.float64)

@@ -553,6 +553,9 @@ __device__ void finalize_scalars(const double (&acc)[6], DevState *st) {
     st->sigma = sg;
   }
   const double eta = fmax(eta_p, fmax(eta_d, eta_g));
+  if (eta <= 1e-4 && st->iter_eta[0] == 0) st->iter_eta[0] = st->iter;
+  if (eta <= 1e-5 && st->iter_eta[1] == 0) st->iter_eta[1] = st->iter;
+  if (eta <= 1e-6 && st->iter_eta[2] == 0) st->iter_eta[2] = st->iter;
   st->eig_warm_valid = 1;   // every block's eigenbasis was stored by this iteration
   st->w_valid = 1;          // Step 3 stored AC - A S^{k+1} for every row
   if ((st->tol >= 0.0 && eta <= st->tol) || st->nan_flag) st->done = 1;
@@ -1854,6 +1857,24 @@ static strom_status set_start_impl(strom_admm *h, const double *X, const double 
   return recompute_products(h);
 }
 
+strom_status strom_admm_reconfigure(strom_admm *h, const strom_admm_config *cfg) {
+  if (!h || !cfg) { set_error("strom_admm_reconfigure: NULL argument"); return STROM_EINVAL; }
+  if (!(cfg->sigma > 0.0) || !(cfg->tau > 0.0 && cfg->tau < 2.0) || cfg->eig_max_sweeps <= 0) {
+    set_error("strom_admm_reconfigure: need sigma > 0, tau in (0,2), eig_max_sweeps > 0");
+    return STROM_EINVAL;
+  }
+  // sigma, tau, the sigma policy and the eigensolver knobs; eps and check_every are fixed
+  // by setup (the factor and the captured graphs depend on them)
+  strom_admm_config c = h->cfg;
+  c.sigma = cfg->sigma; c.tau = cfg->tau; c.sigma_period = cfg->sigma_period;
+  c.sigma_ratio = cfg->sigma_ratio; c.sigma_factor = cfg->sigma_factor;
+  c.sigma_min = cfg->sigma_min; c.sigma_max = cfg->sigma_max;
+  c.eig_max_sweeps = cfg->eig_max_sweeps; c.eig_tol = cfg->eig_tol;
+  c.eig_warm = cfg->eig_warm; c.eig_cold_every = cfg->eig_cold_every;
+  h->cfg = c;
+  return STROM_OK;
+}
+
 strom_status strom_admm_set_start(strom_admm *h, const double *X, const double *y, const double *S) {
   if (!h) { set_error("strom_admm_set_start: NULL handle"); return STROM_EINVAL; }
   return set_start_impl(h, X, y, S, cudaMemcpyHostToDevice);
@@ -1937,6 +1958,7 @@ strom_status strom_admm_get(strom_admm *h, double *X, double *y, double *S, stro
     res->iter = ds.iter; res->eta_p = ds.eta_p; res->eta_d = ds.eta_d; res->eta_g = ds.eta_g;
     res->pobj = ds.pobj; res->dobj = ds.dobj; res->sigma = ds.sigma_used; res->eta_x = ds.eta_x;
     res->eig_sweeps = (int64_t)ds.eig_sweeps;
+    for (int k = 0; k < 3; ++k) res->iter_eta[k] = ds.iter_eta[k];
   }
   if (ds.eig_fail) {
     set_error("Jacobi sweep cap reached on block " + std::to_string(ds.eig_fail - 1));

@@ -24,6 +24,7 @@ struct DevState {          // scalars living on the device
   double sigma_ratio, sigma_factor, sigma_min, sigma_max;
   // residuals of the latest completed iterate
   double eta_p, eta_d, eta_g, pobj, dobj, eta_x, sigma_used;
+  int64_t iter_eta[3];     // first iteration with eta <= 1e-4, 1e-5, 1e-6 (0 = not yet)
 };
 
 // r_i = (b_i - AX_i) / sigma + (AC_i - (A S)_i) : Step 1/3 right-hand side

@@ -484,6 +484,11 @@ def test_final_objective_and_certificate_parity(name, state, policy):
     it_o, ok_o = o.solve_to_tol(1e-6, 5000)
     assert ok_g and ok_o and it_g == it_o, (it_g, it_o)
     X, y, Sg, res = g.get()
+    # the device's first-crossing marks agree with the oracle's trace
+    for tol, key in ((1e-4, "1e-4"), (1e-5, "1e-5"), (1e-6, "1e-6")):
+        first = next(i + 1 for i in range(len(o.trace.eta_p))
+                     if max(o.trace.eta_p[i], o.trace.eta_d[i], o.trace.eta_g[i]) <= tol)
+        assert res["iter_eta"][key] == first, (key, res["iter_eta"][key], first)
     ep, ed, eg, po, do = o.residuals()
     for a, b in ((res["pobj"], po), (res["dobj"], do), (o.b @ y, do)):
         assert abs(a - b) <= 1e-6 * max(1.0, abs(b)), (a, b)
