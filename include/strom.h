@@ -220,6 +220,11 @@ strom_status strom_batch_iterate(strom_batch *b, int64_t iters);
 strom_status strom_batch_solve(strom_batch *b, double tol, int64_t maxiter, int64_t *iters_done,
                                int32_t *converged);
 
+/* Wall-clock milliseconds of the setup phases of a handle: ms[0] host factorisation
+ * (build_factor: AA*, leaf groups, K'), ms[1] uploads, ms[2] device dense factors
+ * (cuSOLVER/cuBLAS), ms[3] eigensolver classes and state, ms[4] graph capture. */
+strom_status strom_admm_setup_times(const strom_admm *h, double *ms);
+
 /* Number of kernel launches one iteration issues (for launch accounting). */
 int32_t strom_admm_launches_per_iter(const strom_admm *h);
 /* Size of the factor data on the device in bytes, and unique dense factors. */

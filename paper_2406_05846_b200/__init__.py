@@ -34,7 +34,7 @@ EXPORTS = [
     "strom_debug_eps", "strom_debug_link_virtual", "strom_debug_iterate_virtual",
     "strom_debug_host_part", "strom_debug_setup_virtual",
     "strom_batch_create", "strom_batch_destroy", "strom_batch_iterate", "strom_batch_solve",
-    "strom_admm_reconfigure",
+    "strom_admm_reconfigure", "strom_admm_setup_times",
 ]
 
 
@@ -100,6 +100,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "strom_admm_destroy": (None, [VP]),
         "strom_admm_set_start": (I32, [VP, P(D), P(D), P(D)]),
         "strom_admm_reconfigure": (I32, [VP, P(strom_admm_config)]),
+        "strom_admm_setup_times": (I32, [VP, P(D)]),
         "strom_admm_set_start_device": (I32, [VP, VP, VP, VP]),
         "strom_admm_iterate": (I32, [VP, I64]),
         "strom_admm_solve": (I32, [VP, D, I64, P(I64)]),
@@ -393,6 +394,12 @@ class StromAdmm:
         if cnt < 0:
             _check(cnt, "strom_admm_kernel_times")
         return [(names[i].decode(), float(ms[i])) for i in range(min(cnt, cap))]
+
+    def setup_times(self):
+        """Setup phases in ms (strom_admm_setup_times)."""
+        ms = np.zeros(5)
+        _check(load().strom_admm_setup_times(self.handle, _dptr(ms)), "strom_admm_setup_times")
+        return dict(zip(("host_factor", "uploads", "device_factor", "eig_state", "graph_capture"), ms.tolist()))
 
     def launches_per_iter(self) -> int:
         return int(load().strom_admm_launches_per_iter(self.handle))

@@ -18,6 +18,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
@@ -697,6 +698,7 @@ struct strom_admm {
   int xfer = 0;                              // 0 single, 1 NCCL ranks, 2 in-process virtual ranks
   ncclComm_t comm = nullptr;
   bool part = false;                         // horizon partition active (nranks > 1)
+  double setup_ms[5] = {0, 0, 0, 0, 0};      // host factor, uploads, device factor, rest, graphs
   PartPlan plan;
   std::vector<PartPlan> plans;               // every rank's plan (gathers in get())
   PartDev pd{};
@@ -1493,6 +1495,15 @@ strom_status device_factor_dense(strom_admm *h, std::vector<const double *> &Lin
 extern "C" {
 
 }  // extern "C"
+// wall-clock phases of setup (strom_admm_setup_times)
+struct SetupClock {
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void lap(double &ms) {
+    const auto now = std::chrono::steady_clock::now();
+    ms = std::chrono::duration<double, std::milli>(now - t).count();
+    t = now;
+  }
+};
 // xfer: 0 one GPU, 1 NCCL ranks, 2 in-process virtual ranks (tests)
 static strom_status setup_impl(strom_admm **out, const strom_sdp *sdp_h, const strom_admm_config *cfg,
                                int device, void *cuda_stream, const void *nccl_unique_id, int rank,
@@ -1523,7 +1534,9 @@ static strom_status setup_impl(strom_admm **out, const strom_sdp *sdp_h, const s
   h->device = device;
   h->m = s.m; h->n = s.n; h->nblocks = s.nblocks;
   h->K = cfg->check_every;
+  SetupClock clk;
   strom_status st = build_factor(s, cfg->eps_rel, cfg->eps, h->F);
+  clk.lap(h->setup_ms[0]);
   if (st != STROM_OK) return st;
   CK(cudaSetDevice(device));
   CK(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device));
@@ -1673,7 +1686,9 @@ static strom_status setup_impl(strom_admm **out, const strom_sdp *sdp_h, const s
   std::vector<int32_t> un(nu), uw(nu);
   double *dTtile = nullptr;
   int nTt = 0;
+  clk.lap(h->setup_ms[1]);
   if ((st = device_factor_dense(h.get(), hLinv, hLinvT, hF, hFt, hH, hHt, un, uw, dTtile, nTt))) return st;
+  clk.lap(h->setup_ms[2]);
   const double **pp1, **pp2, **pp3, **pp4, **pp5, **pp6;
   if ((st = h->upload(pp1, hLinv)) || (st = h->upload(pp2, hLinvT)) || (st = h->upload(pp3, hF)) ||
       (st = h->upload(pp4, hFt)) || (st = h->upload(pp5, hH)) || (st = h->upload(pp6, hHt)) ||
@@ -1815,14 +1830,22 @@ static strom_status setup_impl(strom_admm **out, const strom_sdp *sdp_h, const s
   h->prof_ev.resize(kMaxProfEvents);
   h->prof_names.assign(kMaxProfEvents, nullptr);
   for (auto &e : h->prof_ev) CK(cudaEventCreate(&e));
+  clk.lap(h->setup_ms[3]);
   if (h->xfer != 2) {        // virtual ranks launch directly (strom_debug_iterate_virtual)
     if ((st = capture(h.get(), h->K, h->graphK, h->execK))) return st;
     if ((st = capture(h.get(), 1, h->graph1, h->exec1))) return st;
   }
+  clk.lap(h->setup_ms[4]);
   *out = h.release();
   return STROM_OK;
 }
 extern "C" {
+
+strom_status strom_admm_setup_times(const strom_admm *h, double *ms) {
+  if (!h || !ms) { set_error("strom_admm_setup_times: NULL argument"); return STROM_EINVAL; }
+  for (int k = 0; k < 5; ++k) ms[k] = h->setup_ms[k];
+  return STROM_OK;
+}
 
 strom_status strom_admm_setup(strom_admm **out, const strom_sdp *sdp_h, const strom_admm_config *cfg,
                               int device, void *cuda_stream, const void *nccl_unique_id, int rank,

@@ -177,8 +177,78 @@ def _entry_coef(r: int, c: int) -> float:
     return 1.0 if r == c else _ISQ2
 
 
+class _LazyCanon:
+    """meta["canon"][k] built on first use (the C++ generator does not return the maps)."""
+
+    def __init__(self, pop, kappa):
+        self.pop, self.kappa, self.cache = pop, kappa, {}
+
+    def __getitem__(self, k):
+        if k not in self.cache:
+            self.cache[k] = _CliqueTable(len(self.pop.cliques[k]), self.kappa).canon
+        return self.cache[k]
+
+    def __len__(self):
+        return self.pop.N
+
+
 def compile_relaxation(pop: ChainPop, kappa: int = 2, name: str | None = None,
-                       normalize: bool = True) -> BlockSdp:
+                       normalize: bool = True, engine: str | None = None) -> BlockSdp:
+    """The relaxation as a BlockSdp. engine "cpp" (default when strom_inputs/libstrom_gen.so
+    loads: the C++ generator of NEXT-3, per clique in parallel) or "python" (the reference
+    implementation below; STROM_GEN=python forces it). Both produce identical bytes."""
+    import os
+    engine = engine or os.environ.get("STROM_GEN", "cpp")
+    if engine == "cpp":
+        from . import fastgen
+        if fastgen.available():
+            return _compile_cpp(pop, kappa, name, normalize)
+    return compile_relaxation_py(pop, kappa, name, normalize)
+
+
+def _compile_cpp(pop: ChainPop, kappa: int, name, normalize: bool) -> BlockSdp:
+    from . import fastgen
+    N = pop.N
+    gs = [[(gi.normalized() if normalize else gi) for gi in pop.g[k]] for k in range(N)]
+    hs = [[(hj.normalized() if normalize else hj) for hj in pop.h[k]] for k in range(N)]
+    arr = fastgen.compile_arrays(pop, kappa, gs, hs)
+    basis = [monomial_basis(len(I), kappa) for I in pop.cliques]
+    mom_block, loc_blocks, loc_bases = [], [], []
+    bi = 0
+    for k in range(N):
+        mom_block.append(bi); bi += 1
+        lb, lbas = [], []
+        for gi in gs[k]:
+            lb.append(bi); bi += 1
+            lbas.append(monomial_basis(len(pop.cliques[k]), kappa - ceil(gi.degree() / 2)))
+        loc_blocks.append(lb); loc_bases.append(lbas)
+    R_beta = _trace_bounds(pop, kappa, normalize, gs, [len(B) for B in basis], mom_block, loc_blocks, loc_bases,
+                           len(arr["block_n"]))
+    sdp = BlockSdp(R_beta=R_beta, kappa=kappa, name=name or pop.name, **arr)
+    sdp.meta = {"mom_block": mom_block, "loc_blocks": loc_blocks, "basis": basis, "loc_bases": loc_bases,
+                "canon": _LazyCanon(pop, kappa), "g_normalized": gs, "pop": pop}
+    return sdp
+
+
+def _trace_bounds(pop, kappa, normalize, gs, nM, mom_block, loc_blocks, loc_bases, nblocks):
+    """R_beta (Theorem 2; reading Q17)."""
+    R_beta = np.empty(nblocks)
+    for k in range(pop.N):
+        Rk = max(1.0, float(pop.R[k]))
+        R_beta[mom_block[k]] = nM[k] * Rk ** (2 * kappa)
+        gmax = pop.meta.get("gmax")
+        for i, gi in enumerate(gs[k]):
+            dg = ceil(gi.degree() / 2)
+            if gmax is not None:
+                gm = gmax[k][i] / (pop.g[k][i].max_abs_coef() if normalize else 1.0)
+            else:  # sum |coef| * Rk^deg bounds max g over the box
+                gm = sum(abs(c) * Rk ** sum(a) for a, c in gi.terms.items())
+            R_beta[loc_blocks[k][i]] = max(gm, 0.0) * len(loc_bases[k][i]) * Rk ** (2 * (kappa - dg))
+    return R_beta
+
+
+def compile_relaxation_py(pop: ChainPop, kappa: int = 2, name: str | None = None,
+                          normalize: bool = True) -> BlockSdp:
     """kappa-th order sparse moment relaxation as a standard SDP.
 
     Row families per clique k:
@@ -301,18 +371,8 @@ def compile_relaxation(pop: ChainPop, kappa: int = 2, name: str | None = None,
             C[offM + s] += fa * T.entry_coef[s]
 
     # ---- trace bounds R_beta (Theorem 2; reading Q17) ---
-    R_beta = np.empty(len(block_n))
-    for k in range(N):
-        Rk = max(1.0, float(pop.R[k]))
-        R_beta[mom_block[k]] = tables[k].nM * Rk ** (2 * kappa)
-        gmax = pop.meta.get("gmax")
-        for i, gi in enumerate(gs[k]):
-            dg = ceil(gi.degree() / 2)
-            if gmax is not None:
-                gm = gmax[k][i] / (pop.g[k][i].max_abs_coef() if normalize else 1.0)
-            else:  # sum |coef| * Rk^deg bounds max g over the box
-                gm = sum(abs(c) * Rk ** sum(a) for a, c in gi.terms.items())
-            R_beta[loc_blocks[k][i]] = max(gm, 0.0) * len(loc_bases[k][i]) * Rk ** (2 * (kappa - dg))
+    R_beta = _trace_bounds(pop, kappa, normalize, gs, [T.nM for T in tables], mom_block, loc_blocks,
+                           loc_bases, len(block_n))
 
     sdp = BlockSdp(
         block_n=block_n,

@@ -226,3 +226,25 @@ def test_carback_rollout_is_feasible():
     X = lift_rank1(sdp, z)
     assert np.max(np.abs(_A(sdp) @ X - sdp.b)) <= 1e-12
     assert abs(sdp.C @ X - pop.objective(z)) <= 1e-10 * (1 + abs(pop.objective(z)))
+
+
+# ---------------------------------------------------------------- NEXT-3: C++ generator
+@pytest.mark.parametrize("name", ["toy", "pend5", "pend5k1", "cartpole3", "carback3", "landing3", "flying3"])
+def test_cpp_generator_is_byte_identical(name):
+    """strom_inputs/csrc/gen.cpp (the fast generator, include/strom_gen.h) produces the same
+    SDP bytes as the Python reference compiler for every model (and kappa = 1)."""
+    from strom_inputs import fastgen, paper_models as PM
+    from strom_inputs.relax import compile_relaxation_py
+    fastgen.build()
+    pop, kappa = {"toy": (models.toy(4), 2), "pend5": (models.pendulum(5, 0.3, 1.0), 2),
+                  "pend5k1": (models.pendulum(5, 0.3, 1.0), 1), "cartpole3": (PM.cartpole(N=3), 2),
+                  "carback3": (PM.carback(N=3), 2), "landing3": (PM.landing(N=3), 2),
+                  "flying3": (PM.flying(N=3), 2)}[name]
+    a = compile_relaxation(pop, kappa=kappa, engine="cpp")
+    b = compile_relaxation_py(pop, kappa=kappa)
+    assert a.meta["basis"] == b.meta["basis"] and a.meta["mom_block"] == b.meta["mom_block"]
+    for k in ("block_n", "block_stage", "block_kind", "block_offset", "A_indptr", "A_indices", "A_data",
+              "b", "C", "row_family", "row_stage", "R_beta"):
+        x, y = getattr(a, k), getattr(b, k)
+        assert x.dtype == y.dtype and np.array_equal(x, y), k
+    assert a.meta["canon"][0] == b.meta["canon"][0]
