@@ -16,6 +16,7 @@
 // the separator Schur complement T = K'_SS - sum F_k^T F_k is factored densely.
 // Identical stage blocks (time-invariant dynamics) share one factor.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <numeric>
@@ -240,7 +241,20 @@ bool small_chol_inv(int g, const double *K, double *Kinv, double rel_floor) {
 
 }  // namespace
 
+// STROM_PROF_SETUP=1: wall time of the build_factor phases on stderr
+static std::chrono::steady_clock::time_point g_prof_t;
+static void prof_lap(int phase) {
+  static const bool on = getenv("STROM_PROF_SETUP") != nullptr;
+  if (!on) return;
+  const auto now = std::chrono::steady_clock::now();
+  if (phase > 0)
+    fprintf(stderr, "[strom setup] phase %d: %.1f ms\n", phase - 1,
+            std::chrono::duration<double, std::milli>(now - g_prof_t).count());
+  g_prof_t = now;
+}
+
 strom_status build_factor(const Sdp &s, double eps_rel, double eps_abs, Factor &f) {
+  prof_lap(0);
   const int m = s.m;
   const int P = s.nstages;
   f.m = m; f.P = P;
@@ -270,6 +284,7 @@ strom_status build_factor(const Sdp &s, double eps_rel, double eps_abs, Factor &
         (col_count[s.col[a]] == 1 || col_count[s.col[a + 1]] == 1))
       leaf_cand[i] = 1;
   }
+  prof_lap(0);
   // ---- K = AA* + eps I ----------------------------------------------------
   std::vector<int64_t> Kp; std::vector<int32_t> Ki; std::vector<double> Kv;
   build_AAt(s, Kp, Ki, Kv);
@@ -287,6 +302,7 @@ strom_status build_factor(const Sdp &s, double eps_rel, double eps_abs, Factor &
     const int32_t *p = std::lower_bound(b0, e0, j);
     return (p != e0 && *p == j) ? Kv[p - Ki.data()] : 0.0;
   };
+  prof_lap(1);
   // ---- leaf groups --------------------------------------------------------
   UF uf(s.n);
   for (int i = 0; i < m; ++i)
@@ -320,6 +336,7 @@ strom_status build_factor(const Sdp &s, double eps_rel, double eps_abs, Factor &
     leaf_groups.push_back(g);
     leaf_kinv.push_back(Kinv);
   }
+  prof_lap(2);
   // ---- internal order ------------------------------------------------------
   f.perm.clear(); f.perm.reserve(m);
   f.gptr.assign(1, 0); f.goff.assign(1, 0); f.gKinv.clear();
@@ -356,6 +373,7 @@ strom_status build_factor(const Sdp &s, double eps_rel, double eps_abs, Factor &
   std::vector<int32_t> leaf_group_of(nL);
   for (size_t q = 0; q + 1 < f.gptr.size(); ++q)
     for (int r = f.gptr[q]; r < f.gptr[q + 1]; ++r) leaf_group_of[r] = (int32_t)q;
+  prof_lap(3);
   // ---- G = K_QL K_LL^{-1} (CSR by Q row, leaf internal columns) -----------
   std::vector<std::vector<int32_t>> Gi(nQ);
   std::vector<std::vector<double>> Gv(nQ);
@@ -403,6 +421,7 @@ strom_status build_factor(const Sdp &s, double eps_rel, double eps_abs, Factor &
         f.Gt_col[fl[l]] = nL + qi; f.Gt_val[fl[l]] = f.G_val[t]; fl[l]++;
       }
   }
+  prof_lap(4);
   // ---- K' = K_QQ - G K_LQ, rows restricted to Q (sparse, internal Q index) ---
   std::vector<std::vector<int32_t>> KPi(nQ);
   std::vector<std::vector<double>> KPv(nQ);
@@ -438,12 +457,15 @@ strom_status build_factor(const Sdp &s, double eps_rel, double eps_abs, Factor &
       for (size_t q = 0; q < list.size(); ++q) { KPv[qi][q] = acc[list[q]]; mark[list[q]] = 0; }
     }
   }
+  prof_lap(5);
   // ---- per-stage dense factors with dedup ------------------------------------
   const int S0 = f.R_off[P];
   const int nS = m - S0;
   f.stage_uid.assign(P, -1); f.stage_wl.assign(P, 0); f.stage_wr.assign(P, 0);
-  std::vector<uint64_t> uid_hash;
-  std::vector<Dense> uid_K, uid_B;
+  // Dedup on the sparse rows of K'_{R_k R_k} and K'_{R_k, [S_{k-1} S_k]} (the dense blocks
+  // are built only for unique stages: time-invariant chains have a handful)
+  struct Sig { int nk, wl, wr; std::vector<int32_t> ij; std::vector<double> v; uint64_t h; };
+  std::vector<Sig> uid_sig;
   std::vector<std::vector<int32_t>> stage_cmap(P);
   for (int k = 0; k < P; ++k) {
     const int r0 = f.R_off[k], nk = f.R_off[k + 1] - r0;
@@ -453,35 +475,45 @@ strom_status build_factor(const Sdp &s, double eps_rel, double eps_abs, Factor &
     std::vector<int32_t> &cmap = stage_cmap[k];  // F column -> position in T (0-based in S)
     for (int c = 0; c < wl; ++c) cmap.push_back(f.S_off[k - 1] - S0 + c);
     for (int c = 0; c < wr; ++c) cmap.push_back(f.S_off[k] - S0 + c);
-    Dense Kd; Kd.rows = Kd.cols = nk; Kd.a.assign((size_t)nk * nk, 0.0);
-    Dense Bd; Bd.rows = nk; Bd.cols = wl + wr; Bd.a.assign((size_t)nk * (wl + wr), 0.0);
-    for (int i = 0; i < nk; ++i) {
-      const int qi = r0 + i - nL;
+    Sig sg{nk, wl, wr, {}, {}, 0};
+    for (int i = 0; i < nk; ++i) {               // (row, column code) with code < nk interior,
+      const int qi = r0 + i - nL;                // nk + c the separator column c of [S_{k-1} S_k]
       for (size_t t = 0; t < KPi[qi].size(); ++t) {
         const int qj = KPi[qi][t] + nL;  // absolute internal
-        if (qj >= r0 && qj < r0 + nk) Kd.row(i)[qj - r0] = KPv[qi][t];
-        else if (wl && qj >= f.S_off[k - 1] && qj < f.S_off[k]) Bd.row(i)[qj - f.S_off[k - 1]] = KPv[qi][t];
-        else if (wr && qj >= f.S_off[k] && qj < f.S_off[k + 1]) Bd.row(i)[wl + qj - f.S_off[k]] = KPv[qi][t];
+        int code;
+        if (qj >= r0 && qj < r0 + nk) code = qj - r0;
+        else if (wl && qj >= f.S_off[k - 1] && qj < f.S_off[k]) code = nk + qj - f.S_off[k - 1];
+        else if (wr && qj >= f.S_off[k] && qj < f.S_off[k + 1]) code = nk + wl + qj - f.S_off[k];
         else if (qj < S0) {
           set_error("strom_admm_setup: interior rows of different stages coupled (not a chain)");
           return STROM_EINVAL;
-        }
+        } else continue;
+        sg.ij.push_back(i); sg.ij.push_back(code); sg.v.push_back(KPv[qi][t]);
       }
     }
-    uint64_t h = fnv(Kd.a.data(), Kd.a.size() * 8);
-    h = fnv(Bd.a.data(), Bd.a.size() * 8, h ^ (uint64_t)(wl * 1000003 + wr));
+    sg.h = fnv(sg.ij.data(), sg.ij.size() * 4, fnv(sg.v.data(), sg.v.size() * 8) ^ (uint64_t)(nk * 7919 + wl * 1000003 + wr));
     int found = -1;
-    for (size_t u = 0; u < uid_hash.size(); ++u)
-      if (uid_hash[u] == h && uid_K[u].rows == nk && uid_B[u].cols == wl + wr &&
-          uid_K[u].a == Kd.a && uid_B[u].a == Bd.a && f.stage_wl[k] == wl) {
+    for (size_t u = 0; u < uid_sig.size(); ++u) {
+      const Sig &o = uid_sig[u];
+      if (o.h == sg.h && o.nk == nk && o.wl == wl && o.wr == wr && o.ij == sg.ij &&
+          std::memcmp(o.v.data(), sg.v.data(), sg.v.size() * 8) == 0 && o.v.size() == sg.v.size()) {
         found = (int)u; break;
       }
+    }
     if (found >= 0) { f.stage_uid[k] = found; continue; }
+    Dense Kd; Kd.rows = Kd.cols = nk; Kd.a.assign((size_t)nk * nk, 0.0);
+    Dense Bd; Bd.rows = nk; Bd.cols = wl + wr; Bd.a.assign((size_t)nk * (wl + wr), 0.0);
+    for (size_t t = 0; t < sg.v.size(); ++t) {
+      const int i = sg.ij[2 * t], code = sg.ij[2 * t + 1];
+      if (code < nk) Kd.row(i)[code] = sg.v[t];
+      else Bd.row(i)[code - nk] = sg.v[t];
+    }
     f.stage_uid[k] = (int)f.uK.size();
-    f.uK.push_back(Kd); f.uB.push_back(Bd);
-    uid_hash.push_back(h); uid_K.push_back(std::move(Kd)); uid_B.push_back(std::move(Bd));
+    f.uK.push_back(std::move(Kd)); f.uB.push_back(std::move(Bd));
+    uid_sig.push_back(std::move(sg));
   }
   f.stage_cmap = stage_cmap;
+  prof_lap(6);
   // ---- separator block K'_SS (its Schur complement T is formed by the backend) -----
   f.T0.rows = f.T0.cols = nS; f.T0.a.assign((size_t)nS * nS, 0.0);
   for (int si = 0; si < nS; ++si) {
@@ -491,6 +523,7 @@ strom_status build_factor(const Sdp &s, double eps_rel, double eps_abs, Factor &
       if (qj >= S0) f.T0.row(si)[qj - S0] = KPv[qi][t];
     }
   }
+  prof_lap(8);
   if (getenv("STROM_VERBOSE")) {
     fprintf(stderr, "[strom] m=%d leaf=%d R=%d S=%d stages=%d unique dense=%zu:", m, nL, S0 - nL, nS, P,
             f.uK.size());
