@@ -296,7 +296,12 @@ __device__ __forceinline__ bool gram_orthogonal(const double *U, int ld, int n, 
     for (int r = 0; r < 4; ++r)
 #pragma unroll
       for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
-    for (int k = 0; k < n; ++k) {
+    // rows visited from a thread-dependent start (tid & 7): the threads of a warp read
+    // different columns (stride == 8 mod 16 doubles, i.e. two bank groups) at 8 different
+    // rows, so a load spreads over 16 bank pairs instead of 2 (a 16-way conflict)
+    int k = tid & 7;
+    if (k >= n) k = 0;
+    for (int kk = 0; kk < n; ++kk) {
       double x[4], z[4];
 #pragma unroll
       for (int r = 0; r < 4; ++r) { x[r] = ui[r][k]; z[r] = uj[r][k]; }
@@ -304,6 +309,7 @@ __device__ __forceinline__ bool gram_orthogonal(const double *U, int ld, int n, 
       for (int r = 0; r < 4; ++r)
 #pragma unroll
         for (int c = 0; c < 4; ++c) acc[r][c] = fma(x[r], z[c], acc[r][c]);
+      if (++k == n) k = 0;
     }
 #pragma unroll
     for (int r = 0; r < 4; ++r)

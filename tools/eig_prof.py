@@ -10,6 +10,7 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 lib = os.path.join(ROOT, "tools", "ab", "libstrom_prof.so")
+os.makedirs(os.path.dirname(lib), exist_ok=True)
 os.environ["STROM_LIB"] = lib          # before the package import reads it
 from paper_2406_05846_b200.build import build  # noqa: E402
 
