@@ -180,21 +180,23 @@ __global__ void k_solve_p1(SolveDev d, RhsArgs ra, const DevState *st) {
 // Dedup batched triangular GEMV: one warp per (unique factor, row, chunk of <= 8 stages).
 // mode 0: out[R_k + i] = sum_{j<=i} Linv[i][j] in[R_k + j]      (P2: v = L^{-1} u)
 // mode 1: out[R_k + i] = sum_{j>=i} LinvT[i][j] in[R_k + j]     (P6b: y = L^{-T} t)
-struct GemvItem { int32_t uid, row, list, cnt; };
-// Items with cnt == 1 (a factor used by one stage, e.g. clique 0) come first and get a
-// whole CTA each (split-K); shared factors get one warp per (row, <= 8 stages).
+// One GEMV work item, fully addressed at setup: the factor row in both orientations
+// (L^{-1} row for P2, L^{-T} row for P6') and the interior-vector bases of its <= 8 stages.
+struct GemvItem { const double *m0, *m1; int32_t row, n, cnt, pad; int32_t base[kGemvChunk]; };
+// Items with cnt == 1 and long rows (a factor used by one stage, e.g. clique 0 of the large
+// problems) come first and get a whole CTA each (split-K); the others one warp per
+// (row, <= 8 stages).
 __global__ void __launch_bounds__(256) k_gemv_stage(SolveDev d, const GemvItem *items, int nitems,
-                                                    int nsingle, const int32_t *stage_list, int mode,
-                                                    const double *in, double *out, const DevState *st) {
-  pdl_trigger();                  // item and factor addressing (static) before the wait
+                                                    int nsingle, int mode, const double *in, double *out,
+                                                    const DevState *st) {
+  pdl_trigger();
   __shared__ double sh[32];
   const int lane = threadIdx.x & 31;
   if ((int)blockIdx.x < nsingle) {
-    const GemvItem it = items[blockIdx.x];
-    const int n = d.uid_n[it.uid];
-    const double *M = (mode == 0 ? d.Linv[it.uid] : d.LinvT[it.uid]) + (int64_t)it.row * n;
-    const int jlo = mode == 0 ? 0 : it.row, jhi = mode == 0 ? it.row + 1 : n;
-    const int b0 = d.R_off[stage_list[it.list]];
+    const GemvItem &it = items[blockIdx.x];
+    const double *M = mode == 0 ? it.m0 : it.m1;
+    const int jlo = mode == 0 ? 0 : it.row, jhi = mode == 0 ? it.row + 1 : it.n;
+    const int b0 = it.base[0];
     pdl_wait();
     if (st->done) return;
     const double sum = cta_dot(M, in + b0, jlo, jhi, sh);
@@ -203,17 +205,14 @@ __global__ void __launch_bounds__(256) k_gemv_stage(SolveDev d, const GemvItem *
   }
   const int w = nsingle + (((int)blockIdx.x - nsingle) * (int)blockDim.x + (int)threadIdx.x) / 32;
   if (w >= nitems) return;
-  const GemvItem it = items[w];
-  const int n = d.uid_n[it.uid];
-  const double *M = (mode == 0 ? d.Linv[it.uid] : d.LinvT[it.uid]) + (int64_t)it.row * n;
-  const int jlo = mode == 0 ? 0 : it.row, jhi = mode == 0 ? it.row + 1 : n;
+  const GemvItem &it = items[w];
+  const double *M = mode == 0 ? it.m0 : it.m1;
+  const int row = it.row, cnt = it.cnt;
+  const int jlo = mode == 0 ? 0 : row, jhi = mode == 0 ? row + 1 : it.n;
   int base[kGemvChunk];
   double acc[kGemvChunk];
 #pragma unroll
-  for (int c = 0; c < kGemvChunk; ++c) {
-    base[c] = c < it.cnt ? d.R_off[stage_list[it.list + c]] : 0;
-    acc[c] = 0.0;
-  }
+  for (int c = 0; c < kGemvChunk; ++c) { base[c] = it.base[c]; acc[c] = 0.0; }
   pdl_wait();
   if (st->done) return;
   int j = jlo + lane;
@@ -221,19 +220,19 @@ __global__ void __launch_bounds__(256) k_gemv_stage(SolveDev d, const GemvItem *
     const double m0 = __ldg(M + j), m1 = __ldg(M + j + 32);
 #pragma unroll
     for (int c = 0; c < kGemvChunk; ++c)
-      if (c < it.cnt) acc[c] += m0 * in[base[c] + j] + m1 * in[base[c] + j + 32];
+      if (c < cnt) acc[c] += m0 * in[base[c] + j] + m1 * in[base[c] + j + 32];
   }
   for (; j < jhi; j += 32) {
     const double mij = __ldg(M + j);
 #pragma unroll
     for (int c = 0; c < kGemvChunk; ++c)
-      if (c < it.cnt) acc[c] += mij * in[base[c] + j];
+      if (c < cnt) acc[c] += mij * in[base[c] + j];
   }
 #pragma unroll
   for (int c = 0; c < kGemvChunk; ++c) {
-    if (c < it.cnt) {
+    if (c < cnt) {
       const double s2 = warp_sum(acc[c]);
-      if (lane == 0) out[base[c] + it.row] = s2;
+      if (lane == 0) out[base[c] + row] = s2;
     }
   }
 }
@@ -248,20 +247,11 @@ __global__ void __launch_bounds__(256) k_solve_p3(SolveDev d, const DevState *st
   const int nw = (gridDim.x * blockDim.x) >> 5;
   for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < d.Sl_hi - d.Sl_lo; w += nw) {
     const int s = d.Sl_lo + w;
-    int j = 0;
-    while (j + 1 < d.P - 1 && d.S_off[j + 1] <= s) ++j;   // separator block of s
-    const int c = s - d.S_off[j];
-    // stage j: its right separator is S_j -> column wl_j + c; stage j+1: left -> column c.
-    // A boundary separator gets only the contribution of the handle's own stage.
-    double a0 = 0.0, a1 = 0.0;
-    if (j >= d.stage_lo && j < d.stage_hi) {
-      const int u0 = d.stage_uid[j], n0 = d.uid_n[u0];
-      a0 = warp_dot(d.Ht[u0] + (int64_t)(d.stage_wl[j] + c) * n0, d.u + d.R_off[j], 0, n0, lane);
-    }
-    if (j + 1 >= d.stage_lo && j + 1 < d.stage_hi) {
-      const int u1 = d.stage_uid[j + 1], n1 = d.uid_n[u1];
-      a1 = warp_dot(d.Ht[u1] + (int64_t)c * n1, d.u + d.R_off[j + 1], 0, n1, lane);
-    }
+    // separator S_j: stage j's row (its right separator, column wl_j + c) and stage j+1's
+    // (left, column c) of H^T; a boundary separator gets only the own stage's term (sep_info)
+    const SepRowInfo in = d.sep_info[w];
+    const double a0 = in.h0 ? warp_dot(in.h0, d.u + in.base0, 0, in.n0, lane) : 0.0;
+    const double a1 = in.h1 ? warp_dot(in.h1, d.u + in.base1, 0, in.n1, lane) : 0.0;
     if (lane == 0) d.u[s] -= a0 + a1;
   }
 }
@@ -362,24 +352,21 @@ __global__ void k_pack_sep_tiles(int n, int nT, const double *C, double *tiles) 
 
 // P6'': y_Rk = w_Rk - H_k y_S,adj with w = L_k^{-T} L_k^{-1} u (P6'), H_k = L_k^{-T} F_k
 // (warp per interior row)
-__global__ void k_solve_p6a(SolveDev d, const int32_t *row_stage, double *y, const DevState *st) {
+__global__ void k_solve_p6a(SolveDev d, double *y, const DevState *st) {
   pdl_enter();
   if (st->done) return;
   const int lane = threadIdx.x & 31, nw = (gridDim.x * blockDim.x) >> 5;
   const int nR = d.R_hi - d.R_lo;
   for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nR; w += nw) {
-  const int q = d.R_lo + w;
-  const int k = row_stage[q - d.nL];
-  const int uid = d.stage_uid[k], wk = d.uid_w[uid], wl = d.stage_wl[k];
-  const int i = q - d.R_off[k];
-  const double *Hi = d.H[uid] + (int64_t)i * wk;
-  double acc = 0.0;
-  for (int c = lane; c < wk; c += 32) {
-    const int s = c < wl ? d.S_off[k - 1] + c : d.S_off[k] + (c - wl);
-    acc += __ldg(Hi + c) * y[s];
-  }
-  acc = warp_sum(acc);
-  if (lane == 0) y[q] = d.t[q] - acc;
+    const int q = d.R_lo + w;
+    const IntRowInfo in = d.int_info[w];
+    double acc = 0.0;
+    for (int c = lane; c < in.wk; c += 32) {
+      const int s = c < in.wl ? in.sl0 + c : in.sr0 + (c - in.wl);
+      acc += __ldg(in.hrow + c) * y[s];
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) y[q] = d.t[q] - acc;
   }
 }
 
@@ -391,8 +378,9 @@ __global__ void k_solve_p7(SolveDev d, RhsArgs ra, double *y, const DevState *st
   if (l >= d.L_hi) return;
   const double is = 1.0 / st->sigma;
   const bool usew = ra.w && st->w_valid;
-  const int g = d.leaf_group[l], g0 = d.gptr[g], gs = d.gptr[g + 1] - g0, a = l - g0;
-  const double *Kinv = d.gKinv + d.goff[g] + (int64_t)a * gs;
+  const LeafRowInfo in = d.leaf_info[l - d.L_lo];
+  const int g0 = in.g0, gs = in.gs, a = l - g0;
+  const double *Kinv = d.gKinv + in.kinv + (int64_t)a * gs;
   double s = 0.0;
   for (int c0 = 0; c0 < gs; c0 += 4) {       // leaf groups have <= 4 rows: one pass
     double kv[4], r[4];
@@ -681,9 +669,7 @@ struct strom_admm {
   int32_t *bn = nullptr; int64_t *boff = nullptr;
   DevState *st = nullptr;
   SolveDev sd{};
-  int32_t *row_stage_R = nullptr;
   GemvItem *items = nullptr; int nitems = 0, nsingle = 0;
-  int32_t *stage_list = nullptr;
   std::vector<std::vector<int32_t>> eig_class_blocks;
   std::vector<int32_t *> eig_class_dev;
   std::vector<int> eig_class_np;
@@ -889,11 +875,10 @@ strom_status launch_solve_front(strom_admm *h, const RhsArgs &ra, double *y, int
     const int gg = h->nsingle + ((h->nitems - h->nsingle) * 32 + TB - 1) / TB;
     mark(h, "trsv_p2_stage_Linv");
     CK(launch_k(use_pdl(h, kPdlP2) && nRl + nSl > 0, k_gemv_stage, gg, TB, 0, s, d, (const GemvItem *)h->items,
-                h->nitems, h->nsingle, (const int32_t *)h->stage_list, 0, (const double *)d.u, d.v,
-                (const DevState *)h->st));
+                h->nitems, h->nsingle, 0, (const double *)d.u, d.v, (const DevState *)h->st));
     mark(h, "trsv_p6b_stage_LinvT");
     CK(launch_k(use_pdl(h, kPdlP6b), k_gemv_stage, gg, TB, 0, s, d, (const GemvItem *)h->items, h->nitems, h->nsingle,
-                (const int32_t *)h->stage_list, 1, (const double *)d.v, nSl > 0 ? d.t : y, (const DevState *)h->st));
+                1, (const double *)d.v, nSl > 0 ? d.t : y, (const DevState *)h->st));
     nl += 2;
   }
   CK(cudaGetLastError());
@@ -927,7 +912,7 @@ strom_status launch_solve_back(strom_admm *h, const RhsArgs &ra, double *y, int 
   }
   if (nRl > 0 && nSl > 0) {
     mark(h, "trsv_p6a_stage_H");
-    k_solve_p6a<<<std::min((nRl * 32 + TB - 1) / TB, 8 * h->num_sms), TB, 0, s>>>(d, h->row_stage_R, y, h->st); ++nl;
+    k_solve_p6a<<<std::min((nRl * 32 + TB - 1) / TB, 8 * h->num_sms), TB, 0, s>>>(d, y, h->st); ++nl;
   }
   const int nLl = d.L_hi - d.L_lo;
   if (nLl > 0) {
@@ -1708,11 +1693,7 @@ static strom_status setup_impl(strom_admm **out, const strom_sdp *sdp_h, const s
   CK(cudaMemset(d.v, 0, sizeof(double) * m));
   CK(cudaMemset(d.t, 0, sizeof(double) * m));
   CK(cudaMemset(d.z, 0, sizeof(double) * m));
-  // interior-row -> stage, GEMV work items (dedup: stages sharing a factor)
-  std::vector<int32_t> rsR(d.S0 - d.nL);
-  for (int k = 0; k < F.P; ++k)
-    for (int q = F.R_off[k]; q < F.R_off[k + 1]; ++q) rsR[q - d.nL] = k;
-  std::vector<int32_t> slist;
+  // GEMV work items (dedup: stages sharing a factor), fully addressed
   std::vector<GemvItem> items, multi;
   for (int u = 0; u < nu; ++u) {
     std::vector<int32_t> stg;
@@ -1724,20 +1705,69 @@ static strom_status setup_impl(strom_admm **out, const strom_sdp *sdp_h, const s
     const bool cta_path = stg.size() == 1 && cta_rows > 0 && un[u] >= cta_rows;
     for (size_t c0 = 0; c0 < stg.size(); c0 += kGemvChunk) {
       const int cnt = (int)std::min<size_t>(kGemvChunk, stg.size() - c0);
-      const int li = (int)slist.size();
-      for (int c = 0; c < cnt; ++c) slist.push_back(stg[c0 + c]);
-      for (int i = 0; i < un[u]; ++i) (cta_path ? items : multi).push_back(GemvItem{u, i, li, cnt});   // warp per row
+      for (int i = 0; i < un[u]; ++i) {                     // warp (or CTA) per row
+        GemvItem it{};
+        it.m0 = hLinv[u] + (int64_t)i * un[u];
+        it.m1 = hLinvT[u] + (int64_t)i * un[u];
+        it.row = i; it.n = un[u]; it.cnt = cnt;
+        for (int c = 0; c < kGemvChunk; ++c) it.base[c] = c < cnt ? F.R_off[stg[c0 + c]] : 0;
+        (cta_path ? items : multi).push_back(it);
+      }
     }
   }
   h->nsingle = (int)items.size();
   items.insert(items.end(), multi.begin(), multi.end());
   h->nitems = (int)items.size();
-  if ((st = h->upload(h->row_stage_R, rsR)) || (st = h->upload(h->stage_list, slist))) return st;
   {
     GemvItem *pi = nullptr;
     if ((st = h->alloc(pi, items.size()))) return st;
     if (!items.empty()) CK(h2d(h.get(), pi, items.data(), items.size() * sizeof(GemvItem)));
     h->items = pi;
+  }
+  // per-row addressing of P3 (separators), P6'' (interiors) and P7 (leaves)
+  {
+    const int S0 = d.S0;
+    std::vector<SepRowInfo> si(std::max(pl.sep_hi - pl.sep_lo, 0));
+    for (int sr = pl.sep_lo; sr < pl.sep_hi; ++sr) {
+      int j = 0;
+      while (j + 1 < F.P - 1 && F.S_off[j + 1] <= sr) ++j;
+      const int c = sr - F.S_off[j];
+      SepRowInfo in{nullptr, nullptr, 0, 0, 0, 0};
+      if (j >= pl.stage_lo && j < pl.stage_hi) {
+        const int u0 = F.stage_uid[j];
+        in.h0 = hHt[u0] + (int64_t)(F.stage_wl[j] + c) * un[u0]; in.base0 = F.R_off[j]; in.n0 = un[u0];
+      }
+      if (j + 1 >= pl.stage_lo && j + 1 < pl.stage_hi) {
+        const int u1 = F.stage_uid[j + 1];
+        in.h1 = hHt[u1] + (int64_t)c * un[u1]; in.base1 = F.R_off[j + 1]; in.n1 = un[u1];
+      }
+      if (in.n0 == 0) in.h0 = nullptr;
+      if (in.n1 == 0) in.h1 = nullptr;
+      si[sr - pl.sep_lo] = in;
+    }
+    (void)S0;
+    std::vector<IntRowInfo> ri(std::max(pl.R_hi - pl.R_lo, 0));
+    for (int k = pl.stage_lo; k < pl.stage_hi; ++k) {
+      const int u = F.stage_uid[k];
+      for (int q = F.R_off[k]; q < F.R_off[k + 1]; ++q) {
+        IntRowInfo in{};
+        in.hrow = hH[u] + (int64_t)(q - F.R_off[k]) * uw[u];
+        in.wk = uw[u]; in.wl = F.stage_wl[k];
+        in.sl0 = k >= 1 ? F.S_off[k - 1] : 0;
+        in.sr0 = F.S_off[std::min(k, F.P - 1)];
+        ri[q - pl.R_lo] = in;
+      }
+    }
+    std::vector<LeafRowInfo> li(std::max(pl.leaf_hi - pl.leaf_lo, 0));
+    for (int g = 0; g + 1 < (int)F.gptr.size(); ++g)
+      for (int l = F.gptr[g]; l < F.gptr[g + 1]; ++l)
+        if (l >= pl.leaf_lo && l < pl.leaf_hi) li[l - pl.leaf_lo] = LeafRowInfo{F.gptr[g], F.gptr[g + 1] - F.gptr[g], F.goff[g]};
+    SepRowInfo *psi = nullptr; IntRowInfo *pri = nullptr; LeafRowInfo *pli = nullptr;
+    if ((st = h->alloc(psi, si.size())) || (st = h->alloc(pri, ri.size())) || (st = h->alloc(pli, li.size()))) return st;
+    if (!si.empty()) CK(h2d(h.get(), psi, si.data(), si.size() * sizeof(SepRowInfo)));
+    if (!ri.empty()) CK(h2d(h.get(), pri, ri.data(), ri.size() * sizeof(IntRowInfo)));
+    if (!li.empty()) CK(h2d(h.get(), pli, li.data(), li.size() * sizeof(LeafRowInfo)));
+    d.sep_info = psi; d.int_info = pri; d.leaf_info = pli;
   }
   // ---- eig size classes -----------------------------------------------------
   {

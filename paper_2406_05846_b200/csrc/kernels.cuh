@@ -40,6 +40,16 @@ struct RhsArgs {
   const double *w; double *wout;
 };
 
+// Per-row addressing of the solve phases, precomputed at setup so that no kernel walks a
+// chain of dependent metadata loads (stage of a row -> factor id -> factor pointer ...)
+// before its first data load. P3: separator row s -> the H^T rows of its two stages (null
+// where the stage is another rank's) and their stage vector bases.
+struct SepRowInfo { const double *h0, *h1; int32_t base0, base1, n0, n1; };
+// P6'': interior row -> its H row, width and the two adjacent separator starts
+struct IntRowInfo { const double *hrow; int32_t wk, wl, sl0, sr0; };
+// P7: leaf row -> its group's first row, size and K_g^{-1} row offset
+struct LeafRowInfo { int32_t g0, gs; int64_t kinv; };
+
 struct SolveDev {
   int32_t m, nL, nQ, P, S0, nS;
   // leaf
@@ -62,6 +72,9 @@ struct SolveDev {
   // (SURVEY.md §8(e)): the rank's leaves [L_lo, L_hi), interiors [R_lo, R_hi), separators
   // [Sl_lo, Sl_hi) incl. both boundaries, and its stages [stage_lo, stage_hi).
   int32_t L_lo, L_hi, R_lo, R_hi, Sl_lo, Sl_hi, stage_lo, stage_hi;
+  const SepRowInfo *sep_info;      // [Sl_hi - Sl_lo]
+  const IntRowInfo *int_info;      // [R_hi - R_lo]
+  const LeafRowInfo *leaf_info;    // [L_hi - L_lo]
 };
 
 // Lower-triangular inverse (e.g. the separator L_T^{-1}, n x n) stored as its lower 64x64
