@@ -544,6 +544,9 @@ __global__ void __launch_bounds__(512, 1) k_eig(EigArgs a) {
           const int i = sub + G * c;
           if (i < n) { up[i] = cs * xp[c] - sn * xq[c]; uq[i] = sn * xp[c] + cs * xq[c]; }
         }
+        // every lane of the group read nrm[p], nrm[q] above; order those reads before the
+        // write (the group is converged here: its lanes share valid, ga and the branch)
+        __syncwarp(G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (grp * G)));
         if (sub == 0) {   // exact norms of the rotated pair from the 2x2 Gram matrix
           const double c2 = cs * cs, s2 = sn * sn, csn = 2.0 * cs * sn * ga;
           nrm[p] = c2 * al - csn + s2 * be;
@@ -954,6 +957,7 @@ __global__ void __cluster_dims__(kClusterEig, 1, 1) __launch_bounds__(512, 1) k_
               up[i] = cs * x - sn * y; uq[i] = sn * x + cs * y;
             }
           }
+          __syncwarp(G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (grp * G)));   // nrm reads before the write
           if (sub == 0) {
             const double c2 = cs * cs, s2 = sn * sn, csn = 2.0 * cs * sn * ga;
             nrm[p] = c2 * al - csn + s2 * be;
@@ -1199,6 +1203,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(512, 1) k_eig_cl(Ei
             const int i = sub + G * c;
             if (i < nloc) { up[i] = cs * xp[c] - sn * xq[c]; uq[i] = sn * xp[c] + cs * xq[c]; }
           }
+          __syncwarp(G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (grp * G)));   // nrm reads before the write
           if (sub == 0) {
             const double c2 = cs * cs, s2 = sn * sn, csn = 2.0 * cs * sn * ga;
             nrm[p] = c2 * al - csn + s2 * be;

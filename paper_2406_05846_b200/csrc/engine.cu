@@ -717,10 +717,14 @@ struct strom_admm {
   // per-kernel event instrumentation of one iteration inside the K-graph
   std::vector<cudaEvent_t> prof_ev;
   std::vector<const char *> prof_names;
+  std::vector<cudaEvent_t> prof2_ev;         // (begin, end) pairs around forked-branch kernels
+  std::vector<const char *> prof2_names;
+  int prof2_idx = 0, prof2_count = 0;
   bool prof_capture = false;
   int prof_idx = 0, prof_count = 0;
   ~strom_admm() {
     for (cudaEvent_t e : prof_ev) cudaEventDestroy(e);
+    for (cudaEvent_t e : prof2_ev) cudaEventDestroy(e);
     if (fork_ev) cudaEventDestroy(fork_ev);
     if (sfork_ev) cudaEventDestroy(sfork_ev);
     if (sjoin_ev) cudaEventDestroy(sjoin_ev);
@@ -796,6 +800,20 @@ void mark(strom_admm *h, const char *name) {
   ++h->prof_idx;
 }
 
+// Begin / end event nodes around a kernel on a forked stream of the instrumented iteration.
+void mark2(strom_admm *h, cudaStream_t s, const char *name) {
+  if (!h->prof_capture || h->prof2_idx + 1 >= (int)h->prof2_ev.size()) return;
+  const int k = h->prof2_idx;
+  cudaEventRecordWithFlags(h->prof2_ev[k], s, cudaEventRecordExternal);
+  h->prof2_names[k / 2] = name;
+  h->prof2_idx = k + 1;
+}
+void mark2_end(strom_admm *h, cudaStream_t s) {
+  if (!h->prof_capture || (h->prof2_idx & 1) == 0) return;
+  cudaEventRecordWithFlags(h->prof2_ev[h->prof2_idx], s, cudaEventRecordExternal);
+  ++h->prof2_idx;
+}
+
 // Kernel launch with programmatic stream serialization (PDL) when `pdl`: the kernel may
 // begin (its static prologue) while the previous kernel on the stream is still running.
 template <typename... KArgs, typename... Args>
@@ -851,12 +869,18 @@ strom_status launch_solve_front(strom_admm *h, const RhsArgs &ra, double *y, int
   }
   if (nSl > 0) {
     cudaStream_t s2 = fork ? h->stream2 : s;
+    mark2(h, s2, "fork_trsv_p3_sep_rhs");
     k_solve_p3<<<std::min((nSl + 7) / 8, 4 * h->num_sms), 256, 0, s2>>>(d, h->st); ++nl;
+    mark2_end(h, s2);
     if (!h->part) {
       const TriTiles &T = h->sep_tiles;
       const int ntl = T.nT * (T.nT + 1) / 2;
+      mark2(h, s2, "fork_trsv_p4_sep_LTinv");
       k_sep_tri<<<ntl, 256, 0, s2>>>(T, 0, d.u + d.S0, d.z + d.S0, h->st); ++nl;
+      mark2_end(h, s2);
+      mark2(h, s2, "fork_trsv_p5_sep_LTinvT");
       k_sep_tri<<<ntl, 256, 0, s2>>>(T, 1, d.z + d.S0, y + d.S0, h->st); ++nl;
+      mark2_end(h, s2);
     } else {
       const PartDev &p = h->pd;
       if (p.nI > 0) {            // z_I = T_II^{-1} u_I on a third stream, overlapping the sum
@@ -1088,8 +1112,9 @@ strom_status capture(strom_admm *h, int iters, cudaGraph_t &g, cudaGraphExec_t &
     const bool instrument = (iters == h->K && i == iters - 1 && !h->prof_ev.empty());
     h->prof_capture = instrument;
     h->prof_idx = 0;
+    h->prof2_idx = 0;
     st = launch_iteration(h, nl);
-    if (instrument) h->prof_count = h->prof_idx;
+    if (instrument) { h->prof_count = h->prof_idx; h->prof2_count = h->prof2_idx / 2; }
     h->prof_capture = false;
     h->launches_per_iter = nl;
   }
@@ -1860,6 +1885,9 @@ static strom_status setup_impl(strom_admm **out, const strom_sdp *sdp_h, const s
   h->prof_ev.resize(kMaxProfEvents);
   h->prof_names.assign(kMaxProfEvents, nullptr);
   for (auto &e : h->prof_ev) CK(cudaEventCreate(&e));
+  h->prof2_ev.resize(2 * 16);
+  h->prof2_names.assign(16, nullptr);
+  for (auto &e : h->prof2_ev) CK(cudaEventCreate(&e));
   clk.lap(h->setup_ms[3]);
   if (h->xfer != 2) {        // virtual ranks launch directly (strom_debug_iterate_virtual)
     if ((st = capture(h.get(), h->K, h->graphK, h->execK))) return st;
@@ -2128,8 +2156,15 @@ int32_t strom_admm_kernel_times(strom_admm *h, double *ms, const char **names, i
     if (ms) ms[i] = (e == cudaSuccess) ? (double)t : -1.0;
     if (names) names[i] = h->prof_names[i];
   }
+  // forked-branch kernels (begin/end pairs), after the main-stream ones
+  for (int k = 0; k < h->prof2_count && cnt + k < cap; ++k) {
+    float t = 0.f;
+    cudaError_t e = cudaEventElapsedTime(&t, h->prof2_ev[2 * k], h->prof2_ev[2 * k + 1]);
+    if (ms) ms[cnt + k] = (e == cudaSuccess) ? (double)t : -1.0;
+    if (names) names[cnt + k] = h->prof2_names[k];
+  }
   cudaGetLastError();
-  return cnt;
+  return cnt + h->prof2_count;
 }
 
 strom_status strom_admm_factor_info(const strom_admm *h, int64_t *device_bytes, int32_t *n_leaf_rows,
