@@ -527,18 +527,36 @@ __global__ void __launch_bounds__(512, 1) k_eig(EigArgs a) {
         // shrink u_p.u_q); (cs, sn) are exactly orthogonal to fp64 precision:
         // cos = (1 + t^2)^(-1/2) by MUFU rsqrt + two Newton steps (branch-free).
         const double d = be - al, g2 = 2.0 * ga;
-        const double h2 = fma(d, d, g2 * g2);
-        double rh = rsqrt_approx(h2);
-        rh = rh * fma(-0.5 * h2, rh * rh, 1.5);
-        const double den = fabs(d) + h2 * rh;
-        double rc = rcp_approx(den);
-        rc = rc * fma(-den, rc, 2.0);
-        const double t = (d >= 0.0 ? g2 : -g2) * rc;
-        const double y = fma(t, t, 1.0);
-        double cs = rsqrt_approx(y);
-        cs = cs * fma(-0.5 * y, cs * cs, 1.5);
-        cs = cs * fma(-0.5 * y, cs * cs, 1.5);
-        const double sn = cs * t;
+        double cs, sn;
+        if (fabs(g2) < 1e-3 * fabs(d)) {
+          // small angle (most rotations of a warm-started sweep): with x = g2/|d|,
+          // t = sign(d) x / (1 + sqrt(1 + x^2)) = sign(d) (x/2)(1 - x^2/4 + O(x^4)) to
+          // 1.3e-13 relative, and cos = (1 + t^2)^(-1/2) = 1 - t^2/2 + 3t^4/8 to O(t^6) =
+          // 1e-24: cs^2 + sn^2 = 1 to fp64 precision. One reciprocal instead of three
+          // MUFU + Newton chains.
+          const double ad = fabs(d);
+          double rc = rcp_approx(ad);
+          rc = rc * fma(-ad, rc, 2.0);
+          const double x = g2 * rc, hx = 0.5 * x;
+          const double t0 = hx * fma(-hx, hx, 1.0);
+          const double t = d >= 0.0 ? t0 : -t0;
+          const double t2 = t * t;
+          cs = fma(t2, fma(t2, 0.375, -0.5), 1.0);
+          sn = cs * t;
+        } else {
+          const double h2 = fma(d, d, g2 * g2);
+          double rh = rsqrt_approx(h2);
+          rh = rh * fma(-0.5 * h2, rh * rh, 1.5);
+          const double den = fabs(d) + h2 * rh;
+          double rc = rcp_approx(den);
+          rc = rc * fma(-den, rc, 2.0);
+          const double t = (d >= 0.0 ? g2 : -g2) * rc;
+          const double y = fma(t, t, 1.0);
+          cs = rsqrt_approx(y);
+          cs = cs * fma(-0.5 * y, cs * cs, 1.5);
+          cs = cs * fma(-0.5 * y, cs * cs, 1.5);
+          sn = cs * t;
+        }
 #pragma unroll
         for (int c = 0; c < EPL; ++c) {
           const int i = sub + G * c;
