@@ -40,6 +40,9 @@ for it in (5, 50, iters):
         print(f"iter {it} n={n}: total cycles mean {tot.mean():.0f} max {tot.max()} | sweeps mean "
               f"{sel[:, 7].mean():.2f} max {sel[:, 7].max()} | per-sweep {(d[:, 2] / sel[:, 7]).mean():.0f}")
         print("    " + "  ".join(f"{nm} {d[:, k].mean():.0f}" for k, nm in enumerate(names)))
+        if sel[:, 12:16].any():
+            print("    eig2 round phases (thread 2, cycles per round): loads+2x2 %.0f  producer %.0f  stores+V %.0f  barrier %.0f" % tuple(
+                (sel[:, 12 + k] / np.maximum(sel[:, 7], 1)).mean() for k in range(4)))
         if sel[:, 8].any():
             st0 = sel[:, 0]
             print("    detail (cycles from start): sched %.0f gather %.0f s %.0f staged %.0f Vcopy %.0f product %.0f" % tuple(

@@ -5,7 +5,7 @@ import numpy as np, torch
 import paper_2406_05846_b200 as S
 from strom_inputs import compile_relaxation, models
 torch.cuda.set_device(0)
-for N in (5, 30):
+for N in [int(x) for x in os.environ.get("QT_N", "5,30").split(",")]:
     t0 = time.time()
     sdp = compile_relaxation(models.pendulum(N, 0.1, 0.0))
     t1 = time.time()
