@@ -216,6 +216,14 @@ __global__ void __launch_bounds__(256) k_gemv_stage(SolveDev d, const GemvItem *
   pdl_wait();
   if (st->done) return;
   int j = jlo + lane;
+  for (; j + 96 < jhi; j += 128) {           // four factor loads in flight per lane
+    const double m0 = __ldg(M + j), m1 = __ldg(M + j + 32), m2 = __ldg(M + j + 64), m3 = __ldg(M + j + 96);
+#pragma unroll
+    for (int c = 0; c < kGemvChunk; ++c)
+      if (c < cnt)
+        acc[c] += (m0 * in[base[c] + j] + m1 * in[base[c] + j + 32]) +
+                  (m2 * in[base[c] + j + 64] + m3 * in[base[c] + j + 96]);
+  }
   for (; j + 32 < jhi; j += 64) {
     const double m0 = __ldg(M + j), m1 = __ldg(M + j + 32);
 #pragma unroll
