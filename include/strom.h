@@ -239,6 +239,14 @@ strom_status strom_admm_factor_info(const strom_admm *h, int64_t *device_bytes,
  * number of launches per iteration, or a negative strom_status. */
 int32_t strom_admm_kernel_times(strom_admm *h, double *ms, const char **names, int32_t cap);
 
+/* Algorithmic work of one launch of the kernel marked `name` (a name returned by
+ * strom_admm_kernel_times, e.g. "trsv_p2_stage_Linv", "update_X"): *bytes = the factor
+ * entries it must read once (unique stage factors counted once) plus its input and output
+ * vectors, *flops = its fp64 flops. The K-EIG classes ("eig_classN") are
+ * not listed (their work is sum 10 n^3 over the class's blocks, computed by the caller).
+ * STROM_EINVAL for a NULL argument or an unknown name. Reading only; no device work. */
+strom_status strom_admm_kernel_work(strom_admm *h, const char *name, double *bytes, double *flops);
+
 /* rank 0: fills the 128-byte NCCL unique id to broadcast (e.g. via torch.distributed). */
 strom_status strom_nccl_get_unique_id(void *id128);
 const char *strom_last_error(void);

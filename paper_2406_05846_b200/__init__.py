@@ -29,7 +29,7 @@ EXPORTS = [
     "strom_admm_setup", "strom_admm_destroy", "strom_admm_set_start",
     "strom_admm_set_start_device", "strom_admm_iterate", "strom_admm_solve", "strom_admm_get",
     "strom_admm_get_device", "strom_admm_lower_bound", "strom_admm_extract", "strom_admm_launches_per_iter",
-    "strom_admm_factor_info", "strom_admm_kernel_times", "strom_nccl_get_unique_id", "strom_last_error", "strom_version",
+    "strom_admm_factor_info", "strom_admm_kernel_times", "strom_admm_kernel_work", "strom_nccl_get_unique_id", "strom_last_error", "strom_version",
     "strom_debug_project_psd", "strom_debug_spmv", "strom_debug_solve", "strom_debug_host_solve",
     "strom_debug_eps", "strom_debug_link_virtual", "strom_debug_iterate_virtual",
     "strom_debug_host_part", "strom_debug_setup_virtual",
@@ -111,6 +111,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
         "strom_admm_launches_per_iter": (I32, [VP]),
         "strom_admm_factor_info": (I32, [VP, P(I64), P(I32), P(I32), P(I32)]),
         "strom_admm_kernel_times": (I32, [VP, P(D), P(C.c_char_p), I32]),
+        "strom_admm_kernel_work": (I32, [VP, C.c_char_p, P(D), P(D)]),
         "strom_nccl_get_unique_id": (I32, [VP]),
         "strom_last_error": (C.c_char_p, []),
         "strom_version": (C.c_char_p, []),
@@ -394,6 +395,14 @@ class StromAdmm:
         if cnt < 0:
             _check(cnt, "strom_admm_kernel_times")
         return [(names[i].decode(), float(ms[i])) for i in range(min(cnt, cap))]
+
+    def kernel_work(self, name: str):
+        """(algorithmic bytes, flops) of one launch of the marked kernel `name`
+        (strom_admm_kernel_work); None for a name without a table entry (K-EIG classes)."""
+        b, f = C.c_double(), C.c_double()
+        if load().strom_admm_kernel_work(self.handle, name.encode(), C.byref(b), C.byref(f)) != 0:
+            return None
+        return b.value, f.value
 
     def setup_times(self):
         """Setup phases in ms (strom_admm_setup_times)."""

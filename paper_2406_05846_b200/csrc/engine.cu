@@ -678,6 +678,8 @@ struct strom_admm {
   DevState *st = nullptr;
   SolveDev sd{};
   GemvItem *items = nullptr; int nitems = 0, nsingle = 0;
+  struct KWork { const char *name; double bytes, flops; };
+  std::vector<KWork> kwork;                  // algorithmic work per launch of the marked kernels
   std::vector<std::vector<int32_t>> eig_class_blocks;
   std::vector<int32_t *> eig_class_dev;
   std::vector<int> eig_class_np;
@@ -1802,6 +1804,41 @@ static strom_status setup_impl(strom_admm **out, const strom_sdp *sdp_h, const s
     if (!li.empty()) CK(h2d(h.get(), pli, li.data(), li.size() * sizeof(LeafRowInfo)));
     d.sep_info = psi; d.int_info = pri; d.leaf_info = pli;
   }
+  // ---- algorithmic bytes per launch of each marked kernel (strom_admm_kernel_work) ------
+  // The data each phase must touch once: its factor entries (unique stage factors counted
+  // once, as the dedup kernels read them) plus its input and output vectors. Roofline
+  // denominators of bench.py.
+  {
+    const double nRl = pl.R_hi - pl.R_lo, nSl = pl.sep_hi - pl.sep_lo, nLl = pl.leaf_hi - pl.leaf_lo;
+    double tri = 0.0, hbytes = 0.0, vecR = 0.0;
+    for (int u = 0; u < nu; ++u) {
+      bool used = false;
+      for (int k = pl.stage_lo; k < pl.stage_hi; ++k) used |= F.stage_uid[k] == u;
+      if (!used) continue;
+      tri += 8.0 * un[u] * (un[u] + 1.0) / 2.0;
+      hbytes += 8.0 * un[u] * uw[u];
+    }
+    vecR = 8.0 * nRl;
+    const double gnnz = (double)(F.G_ptr.empty() ? 0 : F.G_ptr.back());
+    const double gtnnz = (double)(F.Gt_ptr.empty() ? 0 : F.Gt_ptr.back());
+    double kinv = 0.0;
+    for (size_t g = 0; g + 1 < F.gptr.size(); ++g) { const double gs = F.gptr[g + 1] - F.gptr[g]; kinv += 8.0 * gs * gs; }
+    const double tiles = h->sep_tiles.nT > 0 ? 8.0 * kSepTile * kSepTile * h->sep_tiles.nT * (h->sep_tiles.nT + 1) / 2.0 : 0.0;
+    const double nnzA = (double)rp[m];
+    const double rhs_row = 8.0 * 4;        // b, A X, A C (or w), out
+    h->kwork = {
+        {"trsv_p1_leaf_fwd", 12.0 * gnnz + rhs_row * (nRl + nSl) + 24.0 * nLl, 2.0 * gnnz},
+        {"trsv_p2_stage_Linv", tri + 2.0 * vecR, 2.0 * (tri / 8.0)},
+        {"trsv_p6b_stage_LinvT", tri + 2.0 * vecR, 2.0 * (tri / 8.0)},
+        {"fork_trsv_p3_sep_rhs", hbytes + vecR + 16.0 * nSl, 2.0 * (hbytes / 8.0)},
+        {"fork_trsv_p4_sep_LTinv", tiles + 16.0 * nSl, 2.0 * tiles / 8.0},
+        {"fork_trsv_p5_sep_LTinvT", tiles + 16.0 * nSl, 2.0 * tiles / 8.0},
+        {"trsv_p6a_stage_H", hbytes + 16.0 * nRl + 8.0 * nSl, 2.0 * (hbytes / 8.0)},
+        {"trsv_p7_leaf_bwd", kinv + 12.0 * gtnnz + rhs_row * nLl + 8.0 * (nRl + nSl), 2.0 * (kinv / 8.0 + gtnnz)},
+        {"update_X", 12.0 * nnzA + 5.0 * 8.0 * (double)h->own_cnt, 2.0 * nnzA},
+        {"spmv_AX_resid", 12.0 * nnzA + 8.0 * ((double)s.n + m), 2.0 * nnzA},
+    };
+  }
   // ---- eig size classes -----------------------------------------------------
   {
     std::vector<int> nps;
@@ -2153,6 +2190,14 @@ strom_status strom_admm_lower_bound(strom_admm *h, const double *R_beta, double 
 }
 
 int32_t strom_admm_launches_per_iter(const strom_admm *h) { return h ? h->launches_per_iter : 0; }
+
+strom_status strom_admm_kernel_work(strom_admm *h, const char *name, double *bytes, double *flops) {
+  if (!h || !name || !bytes || !flops) { set_error("strom_admm_kernel_work: NULL argument"); return STROM_EINVAL; }
+  for (const auto &w : h->kwork)
+    if (std::strcmp(w.name, name) == 0) { *bytes = w.bytes; *flops = w.flops; return STROM_OK; }
+  set_error(std::string("strom_admm_kernel_work: no kernel mark named ") + name);
+  return STROM_EINVAL;
+}
 
 int32_t strom_admm_kernel_times(strom_admm *h, double *ms, const char **names, int32_t cap) {
   if (!h) { set_error("strom_admm_kernel_times: NULL handle"); return STROM_EINVAL; }
