@@ -258,8 +258,26 @@ __global__ void __launch_bounds__(256) k_solve_p3(SolveDev d, const DevState *st
     // separator S_j: stage j's row (its right separator, column wl_j + c) and stage j+1's
     // (left, column c) of H^T; a boundary separator gets only the own stage's term (sep_info)
     const SepRowInfo in = d.sep_info[w];
-    const double a0 = in.h0 ? warp_dot(in.h0, d.u + in.base0, 0, in.n0, lane) : 0.0;
-    const double a1 = in.h1 ? warp_dot(in.h1, d.u + in.base1, 0, in.n1, lane) : 0.0;
+    // both row dots in one loop: eight H loads (and eight u loads) in flight per lane
+    const int n0 = in.h0 ? in.n0 : 0, n1 = in.h1 ? in.n1 : 0;
+    const double *x0 = d.u + in.base0, *x1 = d.u + in.base1;
+    double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0, q0 = 0.0, q1 = 0.0, q2 = 0.0, q3 = 0.0;
+    const int nmax = n0 > n1 ? n0 : n1;
+    for (int j = lane; j < nmax; j += 128) {
+      double h[8], x[8];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int jj = j + 32 * k;
+        h[k] = jj < n0 ? __ldg(in.h0 + jj) : 0.0;
+        x[k] = jj < n0 ? x0[jj] : 0.0;
+        h[4 + k] = jj < n1 ? __ldg(in.h1 + jj) : 0.0;
+        x[4 + k] = jj < n1 ? x1[jj] : 0.0;
+      }
+      p0 += h[0] * x[0]; p1 += h[1] * x[1]; p2 += h[2] * x[2]; p3 += h[3] * x[3];
+      q0 += h[4] * x[4]; q1 += h[5] * x[5]; q2 += h[6] * x[6]; q3 += h[7] * x[7];
+    }
+    const double a0 = warp_sum((p0 + p1) + (p2 + p3));
+    const double a1 = warp_sum((q0 + q1) + (q2 + q3));
     if (lane == 0) d.u[s] -= a0 + a1;
   }
 }

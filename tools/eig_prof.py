@@ -28,7 +28,7 @@ raw = C.CDLL(lib)
 nb = sdp.nblocks
 bn = np.asarray(sdp.block_n)
 names = ["gather", "warm U=AV", "sweeps", "eigpairs", "recon S", "store V"]
-for it in (5, 50, iters):
+for it in (5, 50, iters, 3 * iters):
     g.iterate(it - g.residuals()["iter"] if it > g.residuals()["iter"] else 1)
     st.synchronize()
     buf = np.zeros((nb, 16), dtype=np.int64)
