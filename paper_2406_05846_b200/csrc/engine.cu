@@ -23,6 +23,7 @@
 #include <cmath>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -671,6 +672,22 @@ struct DBuf {
 }  // namespace
 
 // ============================ handle =========================================
+// Device memory of the handles comes from the device's stream-ordered pool, which keeps up
+// to kPoolKeepBytes cached between handles: a re-setup (an MPC step, a grid of
+// instances) reuses the previous handle's memory instead of cudaMalloc/cudaFree calls.
+constexpr uint64_t kPoolKeepBytes = 8ull << 30;
+inline cudaError_t pool_alloc(void **p, size_t bytes, int device, cudaStream_t s) {
+  static std::once_flag once[64];
+  std::call_once(once[device & 63], [device] {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t keep = kPoolKeepBytes;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  });
+  return cudaMallocAsync(p, bytes, s);
+}
+
 struct strom_admm {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -751,6 +768,8 @@ struct strom_admm {
   bool prof_capture = false;
   int prof_idx = 0, prof_count = 0;
   ~strom_admm() {
+    for (cudaStream_t x : {stream, stream2, stream3})     // pending work (an error path) first
+      if (x) cudaStreamSynchronize(x);
     for (cudaEvent_t e : prof_ev) cudaEventDestroy(e);
     for (cudaEvent_t e : prof2_ev) cudaEventDestroy(e);
     if (fork_ev) cudaEventDestroy(fork_ev);
@@ -768,14 +787,17 @@ struct strom_admm {
     if (exec1) cudaGraphExecDestroy(exec1);
     if (graphK) cudaGraphDestroy(graphK);
     if (graph1) cudaGraphDestroy(graph1);
-    for (void *p : allocs) cudaFree(p);
+    if (stream) {                 // back to the device pool, stream-ordered after all work
+      for (void *p : allocs) cudaFreeAsync(p, stream);
+      cudaStreamSynchronize(stream);
+    }
     if (own_stream && stream) cudaStreamDestroy(stream);
   }
   template <class T>
   strom_status alloc(T *&p, size_t count) {
     p = nullptr;
     if (count == 0) count = 1;
-    cudaError_t e = cudaMalloc((void **)&p, count * sizeof(T));
+    cudaError_t e = pool_alloc((void **)&p, count * sizeof(T), device, stream);
     if (e != cudaSuccess) { set_error(std::string("cudaMalloc: ") + cudaGetErrorString(e)); return STROM_ENOMEM; }
     allocs.push_back(p);
     alloc_bytes.push_back(count * sizeof(T));
@@ -789,7 +811,7 @@ struct strom_admm {
     dev_bytes -= (int64_t)alloc_bytes[k];
     allocs.erase(it);
     alloc_bytes.erase(alloc_bytes.begin() + k);
-    cudaFree(p);
+    cudaFreeAsync(p, stream);
   }
   template <class T>
   strom_status upload(T *&p, const std::vector<T> &h) {
@@ -1275,16 +1297,28 @@ __global__ void k_zero_upper_colmajor(int n, double *A) {
 
 namespace {
 
+// cuSOLVER / cuBLAS handles for the setup-only dense factors, created once per (host
+// thread, device) and kept: creating them costs 3-15 ms per setup. Not destroyed at exit
+// (the driver may already be shutting down).
 struct SolverHandles {
   cusolverDnHandle_t sol = nullptr;
   cublasHandle_t blas = nullptr;
   cusolverDnParams_t params = nullptr;
-  ~SolverHandles() {
-    if (params) cusolverDnDestroyParams(params);
-    if (sol) cusolverDnDestroy(sol);
-    if (blas) cublasDestroy(blas);
-  }
 };
+strom_status solver_handles(int device, cudaStream_t s, SolverHandles *&out) {
+  static thread_local SolverHandles cache[64];
+  SolverHandles &H = cache[device & 63];
+  if (!H.sol) {
+    CSOL(cusolverDnCreate(&H.sol));
+    CSOL(cusolverDnCreateParams(&H.params));
+    CBLAS(cublasCreate(&H.blas));
+    CBLAS(cublasSetMathMode(H.blas, CUBLAS_DEFAULT_MATH));
+  }
+  CSOL(cusolverDnSetStream(H.sol, s));
+  CBLAS(cublasSetStream(H.blas, s));
+  out = &H;
+  return STROM_OK;
+}
 
 // in place: A (n x n column-major, symmetric PD) -> L^{-1} (lower, column-major, upper zeroed)
 strom_status chol_inverse(SolverHandles &H, cudaStream_t s, int n, double *A, int *dinfo, const char *what) {
@@ -1297,26 +1331,26 @@ strom_status chol_inverse(SolverHandles &H, cudaStream_t s, int n, double *A, in
   wd = std::max(wd, wd2); wh = std::max(wh, wh2);
   void *dw = nullptr;
   std::vector<char> hw(std::max<size_t>(wh, 1));
-  CK(cudaMalloc(&dw, std::max<size_t>(wd, 8)));
+  CK(cudaMallocAsync(&dw, std::max<size_t>(wd, 8), s));
   int info = 0;
   cusolverStatus_t r1 = cusolverDnXpotrf(H.sol, H.params, CUBLAS_FILL_MODE_LOWER, n, CUDA_R_64F, A, n, CUDA_R_64F,
                                          dw, wd, hw.data(), wh, dinfo);
   cudaError_t e1 = cudaMemcpyAsync(&info, dinfo, sizeof(int), cudaMemcpyDeviceToHost, s);
   cudaError_t e2 = cudaStreamSynchronize(s);
   if (r1 != CUSOLVER_STATUS_SUCCESS || e1 != cudaSuccess || e2 != cudaSuccess) {
-    cudaFree(dw);
+    cudaFreeAsync(dw, s);
     set_error(std::string("potrf failed on ") + what);
     return STROM_ECUDA;
   }
   if (info != 0) {
-    cudaFree(dw);
+    cudaFreeAsync(dw, s);
     set_error(std::string("strom_admm_setup: non-positive pivot ") + std::to_string(info) + " factoring " + what);
     return STROM_EFACTOR;
   }
   cusolverStatus_t r2 = cusolverDnXtrtri(H.sol, CUBLAS_FILL_MODE_LOWER, CUBLAS_DIAG_NON_UNIT, n, CUDA_R_64F, A, n,
                                          dw, wd, hw.data(), wh, dinfo);
+  cudaFreeAsync(dw, s);
   cudaStreamSynchronize(s);
-  cudaFree(dw);
   if (r2 != CUSOLVER_STATUS_SUCCESS) { set_error(std::string("trtri failed on ") + what); return STROM_ECUDA; }
   const int64_t nn = (int64_t)n * n;
   k_zero_upper_colmajor<<<(unsigned)((nn + 255) / 256), 256, 0, s>>>(n, A);
@@ -1444,16 +1478,25 @@ strom_status device_factor_dense(strom_admm *h, std::vector<const double *> &Lin
                                  std::vector<const double *> &Hp, std::vector<const double *> &Htp,
                                  std::vector<int32_t> &un, std::vector<int32_t> &uw, double *&Ttile, int &nTt) {
   const Factor &F = h->F;
-  SolverHandles H;
-  CSOL(cusolverDnCreate(&H.sol));
-  CSOL(cusolverDnSetStream(H.sol, h->stream));
-  CSOL(cusolverDnCreateParams(&H.params));
-  CBLAS(cublasCreate(&H.blas));
-  CBLAS(cublasSetStream(H.blas, h->stream));
-  CBLAS(cublasSetMathMode(H.blas, CUBLAS_DEFAULT_MATH));
-  int *dinfo = nullptr;
-  strom_status st = h->alloc(dinfo, 1);
+  // STROM_PROF_SETUP=1: wall time of the device-factor steps on stderr (stream synchronised)
+  static const bool prof = getenv("STROM_PROF_SETUP") != nullptr;
+  auto t_last = std::chrono::steady_clock::now();
+  auto lap = [&](const char *what) {
+    if (!prof) return;
+    cudaStreamSynchronize(h->stream);
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[strom device factor] %s: %.1f ms\n", what,
+            std::chrono::duration<double, std::milli>(now - t_last).count());
+    t_last = now;
+  };
+  SolverHandles *Hs = nullptr;
+  strom_status st = solver_handles(h->device, h->stream, Hs);
   if (st) return st;
+  SolverHandles &H = *Hs;
+  int *dinfo = nullptr;
+  st = h->alloc(dinfo, 1);
+  if (st) return st;
+  lap("library handles");
   const int nu = (int)F.uK.size();
   std::vector<double *> Fcm(nu, nullptr);   // column-major F (n_k x w) == row-major F^T
   for (int u = 0; u < nu; ++u) {
@@ -1492,6 +1535,7 @@ strom_status device_factor_dense(strom_admm *h, std::vector<const double *> &Lin
     double *Hr = nullptr;
     if ((st = transpose_into(h, w, nk, Hd, Hr))) return st;
     Hp[u] = Hr;
+    lap("stage factor");
   }
   // separator Schur complement T = K'_SS - sum_k F_k^T F_k, then L_T^{-1}
   const int nS = F.T0.rows;
@@ -1513,7 +1557,9 @@ strom_status device_factor_dense(strom_admm *h, std::vector<const double *> &Lin
       CK(cudaStreamSynchronize(h->stream));
       return STROM_OK;
     }
+    lap("separator Schur complement (syrk)");
     if ((st = chol_inverse(H, h->stream, nS, T, dinfo, "the separator Schur complement"))) return st;
+    lap("separator chol + inverse");
     // T holds L_T^{-1} column-major (upper zeroed): pack its lower tiles
     nTt = (nS + kSepTile - 1) / kSepTile;
     const int ntiles = nTt * (nTt + 1) / 2;
