@@ -47,10 +47,17 @@ def main():
     th, thd = a.theta0, a.theta_dot0
     prev, sigma, u_prev = None, 1.0, None
     rows = []
+    # process warm-up (not timed): the first handle of a process loads the cuSOLVER/cuBLAS
+    # kernels (~1-3 s); a controller pays that once at start-up, not per control step
+    S.StromAdmm(S.StromSdp(compile_relaxation(models.pendulum(a.N, th, thd))),
+                S.strom_admm_default_config(check_every=100), stream=stream).iterate(1)
+    stream.synchronize()
     for k in range(a.steps):
+        t_gen = time.perf_counter()
         sdp = compile_relaxation(models.pendulum(a.N, th, thd))
         dt = sdp.meta["pop"].meta["params"].dt
         t0 = time.perf_counter()
+        t_gen = t0 - t_gen
         g = S.StromAdmm(S.StromSdp(sdp), S.strom_admm_default_config(check_every=100, sigma=sigma, **pol),
                         stream=stream)
         if prev is not None and not a.cold:
@@ -69,7 +76,8 @@ def main():
         u_prev = certify.pendulum_controls(z_hat, a.N)
         rows.append({"step": k, "state": [th, thd], "ok": bool(ok), "iters": int(it),
                      "eta": max(r["eta_p"], r["eta_d"], r["eta_g"]), "sigma": r["sigma"],
-                     "xi": xi, "u0": float(u_prev[0]), "solve_s": t_solve, "solve_and_cert_s": t_all})
+                     "xi": xi, "u0": float(u_prev[0]), "generate_s": t_gen, "solve_s": t_solve,
+                     "solve_and_cert_s": t_all, "setup_ms": g.setup_times()})
         print(json.dumps(rows[-1]), flush=True)
         if not a.cold:
             prev, sigma = (X, y, Sm), r["sigma"]
@@ -83,6 +91,8 @@ def main():
            "median_xi": float(np.median(xis)),
            "mean_solve_s": float(np.mean([r["solve_s"] for r in rows])),
            "mean_solve_and_cert_s": float(np.mean([r["solve_and_cert_s"] for r in rows])),
+           "mean_generate_s": float(np.mean([r["generate_s"] for r in rows])),
+           "mean_setup_s": float(np.mean([sum(r["setup_ms"].values()) / 1e3 for r in rows])),
            "mean_iters": float(np.mean([r["iters"] for r in rows])),
            "final_state": [th, thd], "rows": rows}
     print(json.dumps({k: v for k, v in out.items() if k != "rows"}))
