@@ -31,3 +31,44 @@ def test_extract_zbar_recovers_rank_one_point():
     z = models.pendulum_rollout(3, rng.uniform(-0.3, 0.3, 3), 0.5, -1.0)
     zbar = certify.extract_zbar(sdp, lift_rank1(sdp, z))
     assert np.allclose(zbar, z, atol=1e-10)
+
+
+def test_upper_bound_against_brute_force():
+    """An independent pin of the certificate: on pendulum N=3 the
+    controls are searched exhaustively (41^3 grid over [-1, 1]^3, feasible rollouts only,
+    then a local polish from the best grid point). The valid lower bound LB must not exceed
+    the global optimum, and the extraction + local solve of certify must reach it."""
+    from scipy.optimize import minimize
+    N, th0, thd0 = 3, 0.3, 1.0
+    sdp = compile_relaxation(models.pendulum(N, th0, thd0))
+    pop, p = sdp.meta["pop"], sdp.meta["pop"].meta["params"]
+    o = Oracle(sdp)
+    it, ok = o.solve_to_tol(1e-6, 20000)
+    assert ok
+    LB, _ = lower_bound(sdp, o.y, o.apply_At(o.y))
+    p_hat, z_hat, feas = certify.pendulum_upper_bound(sdp, o.X)
+    assert feas
+
+    def J(u):
+        return pop.objective(models.pendulum_rollout(N, u, th0, thd0, p))
+
+    def margin(u):
+        z = models.pendulum_rollout(N, u, th0, thd0, p)
+        return 1.0 - z[[5 * k + 3 for k in range(1, N + 1)]] ** 2 - p.fc_min ** 2
+
+    g = np.linspace(-1.0, 1.0, 41)
+    best, ubest = np.inf, None
+    for a in g:
+        for b in g:
+            for c in g:
+                u = np.array([a, b, c])
+                if np.all(margin(u) >= 0.0):
+                    v = J(u)
+                    if v < best:
+                        best, ubest = v, u
+    res = minimize(J, ubest, method="SLSQP", bounds=[(-1.0, 1.0)] * N,
+                   constraints=[{"type": "ineq", "fun": margin}], options={"ftol": 1e-14, "maxiter": 500})
+    p_star = min(best, res.fun if np.all(margin(res.x) >= -1e-12) else np.inf)
+    assert LB <= p_star + 1e-8 * (1 + abs(p_star)), (LB, p_star)
+    assert p_hat <= p_star + 1e-6 * (1 + abs(p_star)), (p_hat, p_star)
+    assert p_hat >= p_star - 1e-6 * (1 + abs(p_star)), (p_hat, p_star)
