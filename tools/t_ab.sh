@@ -1,5 +1,4 @@
 mkdir -p gpurun_out/ab
-timeout 900 python -m pytest tests -m gpu -q -x -p no:cacheprovider > gpurun_out/ab/pytest_sep2.log 2>&1
-python tools/ab_time.py tools/ab/libA_base.so tools/ab/libB_sep2.so landing50 2 > gpurun_out/ab/ab_sep2_landing50.txt 2>&1
-python tools/ab_time.py tools/ab/libA_base.so tools/ab/libB_sep2.so carback30 2 > gpurun_out/ab/ab_sep2_carback30.txt 2>&1
-python tools/ab_time.py tools/ab/libA_base.so tools/ab/libB_sep2.so 30 3 > gpurun_out/ab/ab_sep2_pend30.txt 2>&1
+timeout 900 python -m pytest tests -m gpu -q -x -p no:cacheprovider > gpurun_out/ab/pytest_dmma.log 2>&1
+for v in 1 0; do STROM_EIG_DMMA=$v timeout 300 python tools/eig_prof.py 30 400 > gpurun_out/ab/prof_dmma$v.log 2>&1; done
+python tools/ab_time.py tools/ab/libB_dmma.so,STROM_EIG_DMMA=0 tools/ab/libB_dmma.so 30 3 > gpurun_out/ab/ab_dmma_pend30.txt 2>&1

@@ -1,2 +1,2 @@
 mkdir -p gpurun_out/micro
-./tools/micro/launch > gpurun_out/micro/launch.txt 2>&1
+./tools/micro/dmma > gpurun_out/micro/dmma.txt 2>&1
