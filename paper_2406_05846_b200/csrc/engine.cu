@@ -126,17 +126,23 @@ __device__ __forceinline__ double warp_dot(const double *__restrict__ a, const d
   return warp_sum((s0 + s1) + (s2 + s3));
 }
 
+// Factor loads: read-only path (L2-resident factors, re-read every iteration), or, for the
+// multi-gigabyte factors of the larger models that stream from HBM, evict-first loads
+// (ld.global.cs) so the streamed factor does not push the solve's vectors out of L2.
+__device__ __forceinline__ double ldf(const double *p, bool stream) { return stream ? __ldcs(p) : __ldg(p); }
+
 // CTA-wide split-K dot (deterministic): all threads of the block cooperate on one row.
 __device__ __forceinline__ double cta_dot(const double *__restrict__ a, const double *__restrict__ x,
-                                          int lo, int hi, double *sh) {
+                                          int lo, int hi, double *sh, bool stream = false) {
   const int nt = blockDim.x, tid = threadIdx.x;
   double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
   int j = lo + tid;
   for (; j + 3 * nt < hi; j += 4 * nt) {
-    const double a0 = __ldg(a + j), a1 = __ldg(a + j + nt), a2 = __ldg(a + j + 2 * nt), a3 = __ldg(a + j + 3 * nt);
+    const double a0 = ldf(a + j, stream), a1 = ldf(a + j + nt, stream), a2 = ldf(a + j + 2 * nt, stream),
+                 a3 = ldf(a + j + 3 * nt, stream);
     s0 += a0 * x[j]; s1 += a1 * x[j + nt]; s2 += a2 * x[j + 2 * nt]; s3 += a3 * x[j + 3 * nt];
   }
-  for (; j < hi; j += nt) s0 += __ldg(a + j) * x[j];
+  for (; j < hi; j += nt) s0 += ldf(a + j, stream) * x[j];
   double v = warp_sum((s0 + s1) + (s2 + s3));
   const int lane = tid & 31, wid = tid >> 5;
   if (lane == 0) sh[wid] = v;
@@ -189,7 +195,7 @@ struct GemvItem { const double *m0, *m1; int32_t row, n, cnt, pad; int32_t base[
 // (row, <= 8 stages).
 __global__ void __launch_bounds__(256) k_gemv_stage(SolveDev d, const GemvItem *items, int nitems,
                                                     int nsingle, int mode, const double *in, double *out,
-                                                    const DevState *st) {
+                                                    const DevState *st, int stream) {
   pdl_trigger();
   __shared__ double sh[32];
   const int lane = threadIdx.x & 31;
@@ -200,7 +206,7 @@ __global__ void __launch_bounds__(256) k_gemv_stage(SolveDev d, const GemvItem *
     const int b0 = it.base[0];
     pdl_wait();
     if (st->done) return;
-    const double sum = cta_dot(M, in + b0, jlo, jhi, sh);
+    const double sum = cta_dot(M, in + b0, jlo, jhi, sh, stream != 0);
     if (threadIdx.x == 0) out[b0 + it.row] = sum;
     return;
   }
@@ -218,7 +224,8 @@ __global__ void __launch_bounds__(256) k_gemv_stage(SolveDev d, const GemvItem *
   if (st->done) return;
   int j = jlo + lane;
   for (; j + 96 < jhi; j += 128) {           // four factor loads in flight per lane
-    const double m0 = __ldg(M + j), m1 = __ldg(M + j + 32), m2 = __ldg(M + j + 64), m3 = __ldg(M + j + 96);
+    const double m0 = ldf(M + j, stream), m1 = ldf(M + j + 32, stream), m2 = ldf(M + j + 64, stream),
+                 m3 = ldf(M + j + 96, stream);
 #pragma unroll
     for (int c = 0; c < kGemvChunk; ++c)
       if (c < cnt)
@@ -226,13 +233,13 @@ __global__ void __launch_bounds__(256) k_gemv_stage(SolveDev d, const GemvItem *
                   (m2 * in[base[c] + j + 64] + m3 * in[base[c] + j + 96]);
   }
   for (; j + 32 < jhi; j += 64) {
-    const double m0 = __ldg(M + j), m1 = __ldg(M + j + 32);
+    const double m0 = ldf(M + j, stream), m1 = ldf(M + j + 32, stream);
 #pragma unroll
     for (int c = 0; c < kGemvChunk; ++c)
       if (c < cnt) acc[c] += m0 * in[base[c] + j] + m1 * in[base[c] + j + 32];
   }
   for (; j < jhi; j += 32) {
-    const double mij = __ldg(M + j);
+    const double mij = ldf(M + j, stream);
 #pragma unroll
     for (int c = 0; c < kGemvChunk; ++c)
       if (c < cnt) acc[c] += mij * in[base[c] + j];
@@ -311,8 +318,8 @@ __global__ void __launch_bounds__(256) k_sep_tri(TriTiles d, int mode, const dou
 #pragma unroll
   for (int k = 0; k < 8; ++k) {             // rows warp*8 + k: 16 loads in flight per lane
     const int r = warp * 8 + k;
-    t0[k] = __ldg(Tt + r * kSepTile + lane);
-    t1[k] = __ldg(Tt + r * kSepTile + lane + 32);
+    t0[k] = ldf(Tt + r * kSepTile + lane, d.stream);
+    t1[k] = ldf(Tt + r * kSepTile + lane + 32, d.stream);
   }
   double *P = d.part + ((int64_t)X * nT + Y) * kSepTile;
   if (mode == 0) {
@@ -713,6 +720,7 @@ struct strom_admm {
   DevState *st = nullptr;
   SolveDev sd{};
   GemvItem *items = nullptr; int nitems = 0, nsingle = 0;
+  bool factor_stream = false;                // stage factors > 256 MB: evict-first factor loads
   struct KWork { const char *name; double bytes, flops; };
   std::vector<KWork> kwork;                  // algorithmic work per launch of the marked kernels
   std::vector<std::vector<int32_t>> eig_class_blocks;
@@ -949,10 +957,10 @@ strom_status launch_solve_front(strom_admm *h, const RhsArgs &ra, double *y, int
     const int gg = h->nsingle + ((h->nitems - h->nsingle) * 32 + TB - 1) / TB;
     mark(h, "trsv_p2_stage_Linv");
     CK(launch_k(use_pdl(h, kPdlP2) && nRl + nSl > 0, k_gemv_stage, gg, TB, 0, s, d, (const GemvItem *)h->items,
-                h->nitems, h->nsingle, 0, (const double *)d.u, d.v, (const DevState *)h->st));
+                h->nitems, h->nsingle, 0, (const double *)d.u, d.v, (const DevState *)h->st, (int)h->factor_stream));
     mark(h, "trsv_p6b_stage_LinvT");
     CK(launch_k(use_pdl(h, kPdlP6b), k_gemv_stage, gg, TB, 0, s, d, (const GemvItem *)h->items, h->nitems, h->nsingle,
-                1, (const double *)d.v, nSl > 0 ? d.t : y, (const DevState *)h->st));
+                1, (const double *)d.v, nSl > 0 ? d.t : y, (const DevState *)h->st, (int)h->factor_stream));
     nl += 2;
   }
   CK(cudaGetLastError());
@@ -1378,6 +1386,13 @@ __global__ void k_gather_sym(const double *T, int nS, const int32_t *rmap, int n
   out[e] = a >= b ? T[(int64_t)b * nS + a] : T[(int64_t)a * nS + b];
 }
 
+// separator tiles above 256 MB stream from HBM every pass: evict-first (STROM_FACTOR_STREAM
+// overrides, as for the stage factors)
+int tile_stream(double bytes) {
+  static const int force = [] { const char *e = getenv("STROM_FACTOR_STREAM"); return e ? atoi(e) : -1; }();
+  return force >= 0 ? force != 0 : bytes > 256.0 * 1024 * 1024;
+}
+
 strom_status alloc_tiles(strom_admm *h, int n, const double *Linv_cm, TriTiles &T) {
   T.n = n;
   T.nT = (n + kSepTile - 1) / kSepTile;
@@ -1388,6 +1403,7 @@ strom_status alloc_tiles(strom_admm *h, int n, const double *Linv_cm, TriTiles &
   if (n > 0) k_pack_sep_tiles<<<ntiles, 256, 0, h->stream>>>(n, T.nT, Linv_cm, tiles);
   CK(cudaGetLastError());
   T.tile = tiles;
+  T.stream = tile_stream((double)ntiles * kSepTile * kSepTile * 8.0);
   if ((st = h->alloc(T.part, (size_t)T.nT * T.nT * kSepTile)) || (st = h->alloc(T.cnt, std::max(T.nT, 1)))) return st;
   CK(cudaMemsetAsync(T.cnt, 0, sizeof(unsigned) * std::max(T.nT, 1), h->stream));
   return STROM_OK;
@@ -1779,7 +1795,8 @@ static strom_status setup_impl(strom_admm **out, const strom_sdp *sdp_h, const s
       (st = h->upload(p_un, un)) || (st = h->upload(p_uw, uw)))
     return st;
   d.Linv = pp1; d.LinvT = pp2; d.F = pp3; d.Ft = pp4; d.H = pp5; d.Ht = pp6; d.uid_n = p_un; d.uid_w = p_uw;
-  h->sep_tiles = TriTiles{dTtile, nTt, d.nS, nullptr, nullptr};
+  h->sep_tiles = TriTiles{dTtile, nTt, d.nS, nullptr, nullptr,
+                          tile_stream((double)nTt * (nTt + 1) / 2 * kSepTile * kSepTile * 8.0)};
   if (nTt > 0) {
     if ((st = h->alloc(h->sep_tiles.part, (size_t)nTt * nTt * kSepTile)) || (st = h->alloc(h->sep_tiles.cnt, nTt)))
       return st;
@@ -1794,6 +1811,12 @@ static strom_status setup_impl(strom_admm **out, const strom_sdp *sdp_h, const s
   CK(cudaMemset(d.z, 0, sizeof(double) * m));
   // GEMV work items (dedup: stages sharing a factor), fully addressed
   std::vector<GemvItem> items, multi;
+  {
+    double tri = 0.0;
+    for (int u = 0; u < nu; ++u) tri += 8.0 * un[u] * (un[u] + 1.0) / 2.0;
+    static const int force = [] { const char *e = getenv("STROM_FACTOR_STREAM"); return e ? atoi(e) : -1; }();
+    h->factor_stream = force >= 0 ? force != 0 : tri > 256.0 * 1024 * 1024;
+  }
   for (int u = 0; u < nu; ++u) {
     std::vector<int32_t> stg;
     for (int k = pl.stage_lo; k < pl.stage_hi; ++k)       // the own stages only

@@ -82,6 +82,7 @@ struct SolveDev {
 // the per-call partial products part[X][Y][64] and per-block arrival counters cnt[nT].
 struct TriTiles {
   const double *tile; int32_t nT, n; double *part; unsigned *cnt;
+  int32_t stream;               // tiles > 256 MB (HBM-streamed): evict-first loads
 };
 
 // Horizon-partitioned separator solve (partition.cpp) on the device, this rank's pieces.
