@@ -720,6 +720,7 @@ struct strom_admm {
   DevState *st = nullptr;
   SolveDev sd{};
   GemvItem *items = nullptr; int nitems = 0, nsingle = 0;
+  bool eig_compact = false;                  // set while a large batch captures its graph
   bool factor_stream = false;                // stage factors > 256 MB: evict-first factor loads
   struct KWork { const char *name; double bytes, flops; };
   std::vector<KWork> kwork;                  // algorithmic work per launch of the marked kernels
@@ -1045,7 +1046,9 @@ strom_status launch_eig(strom_admm *h, int mode, const double *yv, int &nl) {
     a.lam12 = h->lam12_dev; a.vtop = h->vtop_dev; a.toff = h->toff_dev;
     a.Vstore = h->Vstore; a.voff = h->voff;
     a.warm_enable = h->cfg.eig_warm; a.cold_every = h->cfg.eig_cold_every;
-    const int threads = eig_threads(np);
+    // batches whose moment blocks outnumber the SMs: 256-thread K-EIG CTAs, two per SM
+    // (the 512-thread CTA holds the whole register file) -- strom_batch_create
+    const int threads = (h->eig_compact && np <= 64) ? std::min(eig_threads(np), 256) : eig_threads(np);
     const size_t smem = eig_smem_bytes(np);
     cudaStream_t s = (fork && c != h->eig_main_class) ? h->stream2 : h->stream;
     if (s == h->stream) mark(h, eig_names[c < 8 ? c : 7]);
@@ -2388,6 +2391,16 @@ strom_status strom_batch_create(strom_batch **out, strom_admm *const *handles, i
   for (auto &e : b->pre) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   CK(cudaMallocHost(&b->hstate, sizeof(DevState) * count));
   for (strom_admm *h : b->hs) CK(cudaStreamSynchronize(h->stream));
+  // more moment-block CTAs than SMs in the batch: compact (256-thread) K-EIG CTAs, two per SM
+  // (pendulum N=30 grid, B = 8: 11.9K -> 13.2K aggregate iters/s; B = 4: one wave either way)
+  {
+    int64_t ctas = 0;
+    for (strom_admm *h : b->hs)
+      if (!h->eig_class_blocks.empty()) ctas += (int64_t)h->eig_class_blocks[h->eig_main_class].size();
+    static const int force = [] { const char *e = getenv("STROM_BATCH_COMPACT"); return e ? atoi(e) : -1; }();
+    const bool compact = force >= 0 ? force != 0 : ctas > handles[0]->num_sms;
+    for (strom_admm *h : b->hs) h->eig_compact = compact;
+  }
   CK(cudaStreamBeginCapture(b->stream, cudaStreamCaptureModeThreadLocal));
   strom_status st = STROM_OK;
   cudaError_t e = cudaEventRecord(b->fork, b->stream);
@@ -2403,6 +2416,7 @@ strom_status strom_batch_create(strom_batch **out, strom_admm *const *handles, i
   }
   cudaGraph_t graph = nullptr;
   cudaError_t e2 = cudaStreamEndCapture(b->stream, &graph);
+  for (strom_admm *h : b->hs) h->eig_compact = false;     // the handles' own graphs are unchanged
   if (st != STROM_OK || e != cudaSuccess || e2 != cudaSuccess) {
     if (graph) cudaGraphDestroy(graph);
     if (st == STROM_OK) { set_error(std::string("strom_batch_create: capture: ") + cudaGetErrorString(e != cudaSuccess ? e : e2)); st = STROM_ECUDA; }

@@ -587,6 +587,28 @@ def test_partition_path_with_nccl_allreduce_in_graph():
     assert sol[1] == "True" and sol[3] == "True", sol
 
 
+def test_compact_batch_matches_separate_runs():
+    """A batch whose moment blocks outnumber the SMs (6 pendulum N=30 instances: 180
+    order-55 blocks) captures 256-thread K-EIG CTAs, two per SM (strom_batch_create): the
+    iterates agree with separate runs to rounding (the Frobenius-norm reduction has half the
+    warps, so not bitwise) -- 30 iterations within the 1e-9 iterate contract (measured
+    5e-11 on S, whose norm is small)."""
+    grid = models.pendulum_grid()
+    sdps = [compile_relaxation(models.pendulum(30, *grid[(37 * b + 5) % 100])) for b in range(6)]
+    sep = [make(sdp, check_every=10) for sdp in sdps]
+    for g in sep:
+        g.iterate(30)
+    bat = [S.StromAdmm(S.StromSdp(sdp), S.strom_admm_default_config(check_every=10),
+                       stream=torch.cuda.Stream()) for sdp in sdps]
+    B = S.StromBatch(bat, iters_per_launch=10)
+    B.iterate(30)
+    for g, h in zip(sep, bat):
+        a, b = g.get(), h.get()
+        assert b[3]["iter"] == 30
+        for k in (0, 2):
+            assert rel(b[k], a[k]) <= 1e-9, (k, rel(b[k], a[k]))
+
+
 def test_batched_instances_match_separate_runs():
     """NEXT-2: a batch of grid instances in one graph with a branch per
     instance gives bitwise the iterates of separate runs, and batch solve stops every
