@@ -18,6 +18,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cstdlib>
 #include <cmath>
@@ -290,6 +291,50 @@ __global__ void __launch_bounds__(256) k_solve_p3(SolveDev d, const DevState *st
   }
 }
 
+// P3, dedup form (single-GPU handles): the stages that share a unique factor share its
+// H^T rows, so one warp takes one H^T row and up to 8 of those stages (the row is read once,
+// not once per stage -- the larger models' H^T does not fit L2). A term of stage k lands in
+// the separator row it belongs to: H^T rows [0, wl_k) feed S_{k-1} as its right-stage term
+// (tB), rows [wl_k, wl_k + wr_k) feed S_k as its left-stage term (tA). The consumer (the
+// first separator pass) reads u_S - (tA + tB): the same two-term sum as k_solve_p3.
+struct P3Item { const double *h; int32_t n, cnt; int32_t in_base[kGemvChunk]; int32_t out[kGemvChunk]; };
+__global__ void __launch_bounds__(256) k_solve_p3d(const P3Item *items, int nitems, const double *u, double *tA,
+                                                   double *tB, const DevState *st) {
+  pdl_enter();
+  if (st->done) return;
+  const int lane = threadIdx.x & 31;
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (w >= nitems) return;
+  const P3Item &it = items[w];
+  const int n = it.n, cnt = it.cnt;
+  int base[kGemvChunk];
+  double acc[kGemvChunk];
+#pragma unroll
+  for (int c = 0; c < kGemvChunk; ++c) { base[c] = it.in_base[c]; acc[c] = 0.0; }
+  const double *H = it.h;
+  int j = lane;
+  for (; j + 96 < n; j += 128) {
+    const double h0 = __ldg(H + j), h1 = __ldg(H + j + 32), h2 = __ldg(H + j + 64), h3 = __ldg(H + j + 96);
+#pragma unroll
+    for (int c = 0; c < kGemvChunk; ++c)
+      if (c < cnt)
+        acc[c] += (h0 * u[base[c] + j] + h1 * u[base[c] + j + 32]) + (h2 * u[base[c] + j + 64] + h3 * u[base[c] + j + 96]);
+  }
+  for (; j < n; j += 32) {
+    const double hj = __ldg(H + j);
+#pragma unroll
+    for (int c = 0; c < kGemvChunk; ++c)
+      if (c < cnt) acc[c] += hj * u[base[c] + j];
+  }
+#pragma unroll
+  for (int c = 0; c < kGemvChunk; ++c) {
+    if (c < cnt) {
+      const double s2 = warp_sum(acc[c]);
+      if (lane == 0) { const int o = it.out[c]; if (o >= 0) tA[o] = s2; else tB[-o - 1] = s2; }
+    }
+  }
+}
+
 // P4 / P5: separator solve T y_S = u_S with the explicit L_T^{-1} stored once, as its
 // lower 64x64 tiles (16.5 MB at pendulum N=30 instead of the 33 MB that separate row-major
 // copies of L_T^{-1} and L_T^{-T} touched, so the whole solve stays L2-resident).
@@ -299,7 +344,8 @@ __global__ void __launch_bounds__(256) k_solve_p3(SolveDev d, const DevState *st
 // (arrival counter) sums them in Y order (deterministic) and re-arms the counter.
 constexpr int kSepTile = 64;
 __global__ void __launch_bounds__(256) k_sep_tri(TriTiles d, int mode, const double *in, double *out,
-                                                 const DevState *st) {
+                                                 const DevState *st, const double *ta = nullptr,
+                                                 const double *tb = nullptr) {
   pdl_enter();
   if (st->done) return;
   __shared__ double colp[8][kSepTile];
@@ -324,7 +370,11 @@ __global__ void __launch_bounds__(256) k_sep_tri(TriTiles d, int mode, const dou
   double *P = d.part + ((int64_t)X * nT + Y) * kSepTile;
   if (mode == 0) {
     const int j0 = J * kSepTile + lane, j1 = j0 + 32;
-    const double x0 = j0 < n ? in[j0] : 0.0, x1 = j1 < n ? in[j1] : 0.0;
+    double x0 = j0 < n ? in[j0] : 0.0, x1 = j1 < n ? in[j1] : 0.0;
+    if (ta) {                                 // u_S - sum of the dedup P3 terms (k_solve_p3d)
+      if (j0 < n) x0 -= ta[j0] + tb[j0];
+      if (j1 < n) x1 -= ta[j1] + tb[j1];
+    }
     double rowv[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) rowv[k] = warp_sum(t0[k] * x0 + t1[k] * x1);
@@ -720,6 +770,8 @@ struct strom_admm {
   DevState *st = nullptr;
   SolveDev sd{};
   GemvItem *items = nullptr; int nitems = 0, nsingle = 0;
+  P3Item *p3items = nullptr; int np3 = 0;    // dedup P3 (single-GPU handles)
+  double *p3tA = nullptr, *p3tB = nullptr;   // its left- and right-stage terms per separator row
   bool eig_compact = false;                  // set while a large batch captures its graph
   bool factor_stream = false;                // stage factors > 256 MB: evict-first factor loads
   struct KWork { const char *name; double bytes, flops; };
@@ -929,13 +981,19 @@ strom_status launch_solve_front(strom_admm *h, const RhsArgs &ra, double *y, int
   if (nSl > 0) {
     cudaStream_t s2 = fork ? h->stream2 : s;
     mark2(h, s2, "fork_trsv_p3_sep_rhs");
-    k_solve_p3<<<std::min((nSl + 7) / 8, 4 * h->num_sms), 256, 0, s2>>>(d, h->st); ++nl;
+    const bool dedup = !h->part && h->np3 > 0;
+    if (dedup)
+      k_solve_p3d<<<(h->np3 * 32 + 255) / 256, 256, 0, s2>>>(h->p3items, h->np3, d.u, h->p3tA, h->p3tB, h->st);
+    else
+      k_solve_p3<<<std::min((nSl + 7) / 8, 4 * h->num_sms), 256, 0, s2>>>(d, h->st);
+    ++nl;
     mark2_end(h, s2);
     if (!h->part) {
       const TriTiles &T = h->sep_tiles;
       const int ntl = T.nT * (T.nT + 1) / 2;
       mark2(h, s2, "fork_trsv_p4_sep_LTinv");
-      k_sep_tri<<<ntl, 256, 0, s2>>>(T, 0, d.u + d.S0, d.z + d.S0, h->st); ++nl;
+      k_sep_tri<<<ntl, 256, 0, s2>>>(T, 0, d.u + d.S0, d.z + d.S0, h->st, dedup ? (const double *)h->p3tA : nullptr,
+                                     dedup ? (const double *)h->p3tB : nullptr); ++nl;
       mark2_end(h, s2);
       mark2(h, s2, "fork_trsv_p5_sep_LTinvT");
       k_sep_tri<<<ntl, 256, 0, s2>>>(T, 1, d.z + d.S0, y + d.S0, h->st); ++nl;
@@ -1893,6 +1951,51 @@ static strom_status setup_impl(strom_admm **out, const strom_sdp *sdp_h, const s
     if (!ri.empty()) CK(h2d(h.get(), pri, ri.data(), ri.size() * sizeof(IntRowInfo)));
     if (!li.empty()) CK(h2d(h.get(), pli, li.data(), li.size() * sizeof(LeafRowInfo)));
     d.sep_info = psi; d.int_info = pri; d.leaf_info = pli;
+  }
+  // ---- dedup P3 items (single-GPU handles; STROM_P3_DEDUP=0 keeps the row-per-warp P3) --
+  if (!h->part && d.nS > 0) {
+    static const int on = [] { const char *e = getenv("STROM_P3_DEDUP"); return e ? atoi(e) : 1; }();
+    if (on) {
+      // stages grouped by (unique factor, wl, wr): their H^T rows mean the same separator rows
+      std::vector<std::array<int32_t, 3>> keys;
+      std::vector<std::vector<int32_t>> groups;
+      for (int k = 0; k < F.P; ++k) {
+        const int u = F.stage_uid[k];
+        if (u < 0 || un[u] == 0 || uw[u] == 0) continue;
+        const std::array<int32_t, 3> key{u, F.stage_wl[k], F.stage_wr[k]};
+        auto it = std::find(keys.begin(), keys.end(), key);
+        if (it == keys.end()) { keys.push_back(key); groups.push_back({k}); }
+        else groups[it - keys.begin()].push_back(k);
+      }
+      std::vector<P3Item> p3;
+      for (size_t gi = 0; gi < keys.size(); ++gi) {
+        const int u = keys[gi][0], wl = keys[gi][1], wr = keys[gi][2];
+        const auto &stg = groups[gi];
+        for (size_t c0 = 0; c0 < stg.size(); c0 += kGemvChunk) {
+          const int cnt = (int)std::min<size_t>(kGemvChunk, stg.size() - c0);
+          for (int rho = 0; rho < wl + wr; ++rho) {
+            P3Item it{};
+            it.h = hHt[u] + (int64_t)rho * un[u];
+            it.n = un[u]; it.cnt = cnt;
+            for (int c = 0; c < kGemvChunk; ++c) {
+              if (c >= cnt) { it.in_base[c] = 0; it.out[c] = 0; continue; }
+              const int k = stg[c0 + c];
+              it.in_base[c] = F.R_off[k];
+              // rho < wl: left separator S_{k-1} (right-stage term -> tB); else S_k (tA)
+              it.out[c] = rho < wl ? -(F.S_off[k - 1] + rho - d.S0) - 1 : F.S_off[k] + (rho - wl) - d.S0;
+            }
+            p3.push_back(it);
+          }
+        }
+      }
+      if (!p3.empty()) {
+        if ((st = h->upload(h->p3items, p3)) || (st = h->alloc(h->p3tA, d.nS)) || (st = h->alloc(h->p3tB, d.nS)))
+          return st;
+        CK(cudaMemsetAsync(h->p3tA, 0, sizeof(double) * d.nS, h->stream));
+        CK(cudaMemsetAsync(h->p3tB, 0, sizeof(double) * d.nS, h->stream));
+        h->np3 = (int)p3.size();
+      }
+    }
   }
   // ---- algorithmic bytes per launch of each marked kernel (strom_admm_kernel_work) ------
   // The data each phase must touch once: its factor entries (unique stage factors counted

@@ -309,8 +309,8 @@ def test_horizon_partition_virtual_ranks(name, P):
     ranks on one device with the multi-GPU kernels: each rank projects and updates only its
     own stages' blocks, solves its rows down to the boundary separators, and the three sums
     per iteration run as device kernels in place of the NCCL allreduces. The gathered
-    iterate equals the single-GPU run to rounding (the partitioned separator solve
-    reassociates: <= 1e-12 relative), every rank holds the same iterate and takes the same
+    iterate equals the single-GPU run to rounding (the partitioned separator solve and the
+    dedup P3 reassociate: <= 1e-10 relative), every rank holds the same iterate and takes the same
     eta / termination decisions, and the result matches the oracle."""
     from strom_inputs.paper_models import paper_instance
     sdp = (compile_relaxation(paper_instance("carback", 8, seed=5)) if name == "carback8" else case(name))
@@ -320,15 +320,17 @@ def test_horizon_partition_virtual_ranks(name, P):
     S.strom_debug_iterate_virtual(ranks, 12)
     Xr, yr, Sr, rr = ref.get()
     outs = [g.get() for g in ranks]
-    # Rounding only: the partitioned separator solve eliminates in a different order (measured
-    # 1.3e-12 on A*y, 1.5e-12 on S after 12 iterations), hence 1e-11. S = (Pi(X_b) - X_b)/sigma
+    # Rounding only: the partitioned separator solve eliminates in a different order, and the
+    # single-GPU reference sums P3 per shared H^T row (k_solve_p3d) while the ranks sum it per
+    # separator row (measured up to 1.0e-11 on X, 1.4e-11 on S after 12 iterations on the
+    # wide190 shape), hence 1e-10, two decades inside the 1e-9 contract. S = (Pi(X_b) - X_b)/sigma
     # carries the eigensolver's rounding in units of ||X_b||, so its difference is measured
     # against ||X|| + ||S|| (||S|| alone can be much smaller).
     scale = np.linalg.norm(Xr) + np.linalg.norm(Sr)
     o_At = compile_At(sdp)
     for X, y, Sg, r in outs:
-        assert rel(X, Xr) <= 1e-11 and np.linalg.norm(Sg - Sr) <= 1e-11 * scale, (rel(X, Xr), rel(Sg, Sr))
-        assert rel(o_At @ y, o_At @ yr) <= 1e-11
+        assert rel(X, Xr) <= 1e-10 and np.linalg.norm(Sg - Sr) <= 1e-10 * scale, (rel(X, Xr), rel(Sg, Sr))
+        assert rel(o_At @ y, o_At @ yr) <= 1e-10
         assert r["iter"] == rr["iter"] == 12
         for k in ("eta_p", "eta_d", "eta_g", "pobj", "dobj"):
             assert abs(r[k] - rr[k]) <= 1e-10 * max(abs(rr[k]), 1e-6), (k, r[k], rr[k])
