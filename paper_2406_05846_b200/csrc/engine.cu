@@ -419,6 +419,140 @@ __global__ void __launch_bounds__(256) k_sep_tri(TriTiles d, int mode, const dou
   if (threadIdx.x == 0) d.cnt[X] = 0u;
 }
 
+// Chunked form for the HBM-streamed separator factors of the larger models: a CTA takes one
+// output block X and a chunk of up to d.yc (16) consecutive input blocks Y (work list
+// d.work[mode]: (X, first Y)), two tiles in flight; the partial sums, arrival counters and
+// the last CTA's sum shrink by the chunk length. Same contract as k_sep_tri.
+__global__ void __launch_bounds__(256) k_sep_tri_chunk(TriTiles d, int mode, const double *in, double *out,
+                                                       const DevState *st, const double *ta = nullptr,
+                                                       const double *tb = nullptr) {
+  pdl_enter();
+  if (st->done) return;
+  __shared__ double colp[8][kSepTile];
+  __shared__ int last;
+  const int nT = d.nT, yc = d.yc, n = d.n;
+  int X, Y0;
+  if (yc == 1) {
+    const int b = blockIdx.x;
+    int I = (int)((sqrtf(8.0f * (float)b + 1.0f) - 1.0f) * 0.5f);
+    while (I * (I + 1) / 2 > b) --I;
+    while ((I + 1) * (I + 2) / 2 <= b) ++I;
+    const int J = b - I * (I + 1) / 2;
+    X = mode == 0 ? I : J; Y0 = mode == 0 ? J : I;
+  } else {
+    const int2 wk = d.work[mode][blockIdx.x];
+    X = wk.x; Y0 = wk.y;
+  }
+  const int ylo = mode == 0 ? 0 : X, yhi = mode == 0 ? X + 1 : nT;     // input blocks of X
+  const int Y1 = min(Y0 + yc, yhi);
+  const int chunk = (Y0 - ylo) / yc, need = (yhi - ylo + yc - 1) / yc;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double acc[8], c0 = 0.0, c1 = 0.0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) acc[k] = 0.0;
+  for (int Y = Y0; Y < Y1; Y += 2) {
+    double t0[2][8], t1[2][8];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const bool ok = Y + u < Y1;               // the second tile only when the chunk has one
+      const int Yu = ok ? Y + u : Y;
+      const int I = mode == 0 ? X : Yu, J = mode == 0 ? Yu : X;
+      const double *Tt = d.tile + ((int64_t)I * (I + 1) / 2 + J) * kSepTile * kSepTile;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int r = warp * 8 + k;
+        t0[u][k] = ok ? ldf(Tt + r * kSepTile + lane, d.stream) : 0.0;
+        t1[u][k] = ok ? ldf(Tt + r * kSepTile + lane + 32, d.stream) : 0.0;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      if (Y + u >= Y1) break;
+      const int Yu = Y + u;
+      if (mode == 0) {                          // row dots: T_XY x_Y
+        const int j0 = Yu * kSepTile + lane, j1 = j0 + 32;
+        double x0 = j0 < n ? in[j0] : 0.0, x1 = j1 < n ? in[j1] : 0.0;
+        if (ta) {                               // u_S - the dedup P3 terms (k_solve_p3d)
+          if (j0 < n) x0 -= ta[j0] + tb[j0];
+          if (j1 < n) x1 -= ta[j1] + tb[j1];
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc[k] += t0[u][k] * x0 + t1[u][k] * x1;
+      } else {                                  // column dots: T_YX^T x_Y
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int i = Yu * kSepTile + warp * 8 + k;
+          const double xi = i < n ? in[i] : 0.0;
+          c0 += t0[u][k] * xi;
+          c1 += t1[u][k] * xi;
+        }
+      }
+    }
+  }
+  double *P = d.part + ((int64_t)X * nT + chunk) * kSepTile;
+  if (mode == 0) {
+    double rowv[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) rowv[k] = warp_sum(acc[k]);
+    if (lane < 8) {
+      double v = rowv[0];
+#pragma unroll
+      for (int k = 1; k < 8; ++k) if (lane == k) v = rowv[k];
+      P[warp * 8 + lane] = v;
+    }
+  } else {
+    colp[warp][lane] = c0; colp[warp][lane + 32] = c1;
+    __syncthreads();
+    if (threadIdx.x < kSepTile) {
+      double v = 0.0;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) v += colp[w][threadIdx.x];
+      P[threadIdx.x] = v;
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(&d.cnt[X], 1u) == (unsigned)(need - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  {
+    const int o = threadIdx.x & (kSepTile - 1), qd = threadIdx.x >> 6;
+    const double *pp = d.part + (int64_t)X * nT * kSepTile + o;
+    double v = 0.0;
+    int c = qd;
+    for (; c + 28 < need; c += 32) {
+      double t[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) t[k] = __ldcg(pp + (int64_t)(c + 4 * k) * kSepTile);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v += t[k];
+    }
+    {
+      double t[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) t[k] = c + 4 * k < need ? __ldcg(pp + (int64_t)(c + 4 * k) * kSepTile) : 0.0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v += t[k];
+    }
+    __syncthreads();
+    colp[qd][o] = v;
+    __syncthreads();
+    if (threadIdx.x < kSepTile) {
+      const int i = X * kSepTile + threadIdx.x;
+      if (i < n) out[i] = (colp[0][o] + colp[1][o]) + (colp[2][o] + colp[3][o]);
+    }
+  }
+  if (threadIdx.x == 0) d.cnt[X] = 0u;
+}
+
+// One separator pass: k_sep_tri (a tile per CTA) or, for chunked tiles, k_sep_tri_chunk.
+void sep_pass(const TriTiles &T, int mode, const double *in, double *out, const DevState *st, cudaStream_t s,
+              const double *ta = nullptr, const double *tb = nullptr) {
+  if (T.yc > 1) k_sep_tri_chunk<<<T.nwork[mode], 256, 0, s>>>(T, mode, in, out, st, ta, tb);
+  else k_sep_tri<<<T.nwork[mode], 256, 0, s>>>(T, mode, in, out, st, ta, tb);
+}
+
 // setup: lower 64x64 tiles of the lower-triangular matrix C (column-major nS x nS)
 __global__ void k_pack_sep_tiles(int n, int nT, const double *C, double *tiles) {
   const int b = blockIdx.x;
@@ -990,22 +1124,20 @@ strom_status launch_solve_front(strom_admm *h, const RhsArgs &ra, double *y, int
     mark2_end(h, s2);
     if (!h->part) {
       const TriTiles &T = h->sep_tiles;
-      const int ntl = T.nT * (T.nT + 1) / 2;
       mark2(h, s2, "fork_trsv_p4_sep_LTinv");
-      k_sep_tri<<<ntl, 256, 0, s2>>>(T, 0, d.u + d.S0, d.z + d.S0, h->st, dedup ? (const double *)h->p3tA : nullptr,
-                                     dedup ? (const double *)h->p3tB : nullptr); ++nl;
+      sep_pass(T, 0, d.u + d.S0, d.z + d.S0, h->st, s2, dedup ? (const double *)h->p3tA : nullptr,
+               dedup ? (const double *)h->p3tB : nullptr); ++nl;
       mark2_end(h, s2);
       mark2(h, s2, "fork_trsv_p5_sep_LTinvT");
-      k_sep_tri<<<ntl, 256, 0, s2>>>(T, 1, d.z + d.S0, y + d.S0, h->st); ++nl;
+      sep_pass(T, 1, d.z + d.S0, y + d.S0, h->st, s2); ++nl;
       mark2_end(h, s2);
     } else {
       const PartDev &p = h->pd;
       if (p.nI > 0) {            // z_I = T_II^{-1} u_I on a third stream, overlapping the sum
         CK(cudaEventRecord(h->ev3f, s2));
         CK(cudaStreamWaitEvent(h->stream3, h->ev3f, 0));
-        const int ntl = p.LI.nT * (p.LI.nT + 1) / 2;
-        k_sep_tri<<<ntl, 256, 0, h->stream3>>>(p.LI, 0, d.u + d.S0 + p.I0, p.zI2, h->st);
-        k_sep_tri<<<ntl, 256, 0, h->stream3>>>(p.LI, 1, p.zI2, p.zI, h->st);
+        sep_pass(p.LI, 0, d.u + d.S0 + p.I0, p.zI2, h->st, h->stream3);
+        sep_pass(p.LI, 1, p.zI2, p.zI, h->st, h->stream3);
         CK(cudaEventRecord(h->ev3j, h->stream3));
         nl += 2;
       }
@@ -1039,9 +1171,8 @@ strom_status launch_solve_back(strom_admm *h, const RhsArgs &ra, double *y, int 
     const PartDev &p = h->pd;
     cudaStream_t s2 = fork ? h->stream2 : s;
     if (p.nB > 0) {
-      const int ntl = p.LB.nT * (p.LB.nT + 1) / 2;
-      k_sep_tri<<<ntl, 256, 0, s2>>>(p.LB, 0, p.recv, p.tB, h->st);
-      k_sep_tri<<<ntl, 256, 0, s2>>>(p.LB, 1, p.tB, p.yB, h->st);
+      sep_pass(p.LB, 0, p.recv, p.tB, h->st, s2);
+      sep_pass(p.LB, 1, p.tB, p.yB, h->st, s2);
       nl += 2;
     }
     if (p.nI > 0) CK(cudaStreamWaitEvent(s2, h->ev3j, 0));
@@ -1454,6 +1585,32 @@ int tile_stream(double bytes) {
   return force >= 0 ? force != 0 : bytes > 256.0 * 1024 * 1024;
 }
 
+// Separator passes: a tile per CTA (k_sep_tri) for L2-resident tiles; 16 tiles per CTA
+// (k_sep_tri_chunk) for the HBM-streamed tiles of the larger models (landing N=50: 7,763 ->
+// 7,459, flying robot N=60: 14,081 -> 13,566 us/iter); STROM_SEP_YC overrides.
+strom_status tri_plan(strom_admm *h, TriTiles &T) {
+  const int nT = T.nT;
+  static const int force = [] { const char *e = getenv("STROM_SEP_YC"); return e ? atoi(e) : 0; }();
+  const int yc = force > 0 ? force : (T.stream ? 16 : 1);
+  T.yc = yc;
+  for (int mode = 0; mode < 2; ++mode) {
+    std::vector<int2> w;
+    for (int X = 0; X < nT; ++X) {
+      const int lo = mode == 0 ? 0 : X, hi = mode == 0 ? X + 1 : nT;
+      for (int Y = lo; Y < hi; Y += yc) w.push_back(make_int2(X, Y));
+    }
+    T.nwork[mode] = (int32_t)w.size();
+    T.work[mode] = nullptr;
+    if (yc > 1) {
+      int2 *pw = nullptr;
+      strom_status st;
+      if ((st = h->upload(pw, w))) return st;
+      T.work[mode] = pw;
+    }
+  }
+  return STROM_OK;
+}
+
 strom_status alloc_tiles(strom_admm *h, int n, const double *Linv_cm, TriTiles &T) {
   T.n = n;
   T.nT = (n + kSepTile - 1) / kSepTile;
@@ -1467,7 +1624,7 @@ strom_status alloc_tiles(strom_admm *h, int n, const double *Linv_cm, TriTiles &
   T.stream = tile_stream((double)ntiles * kSepTile * kSepTile * 8.0);
   if ((st = h->alloc(T.part, (size_t)T.nT * T.nT * kSepTile)) || (st = h->alloc(T.cnt, std::max(T.nT, 1)))) return st;
   CK(cudaMemsetAsync(T.cnt, 0, sizeof(unsigned) * std::max(T.nT, 1), h->stream));
-  return STROM_OK;
+  return tri_plan(h, T);
 }
 
 // Setup of the horizon-partitioned separator solve (partition.cpp has the math and a host
@@ -1862,6 +2019,7 @@ static strom_status setup_impl(strom_admm **out, const strom_sdp *sdp_h, const s
     if ((st = h->alloc(h->sep_tiles.part, (size_t)nTt * nTt * kSepTile)) || (st = h->alloc(h->sep_tiles.cnt, nTt)))
       return st;
     CK(cudaMemsetAsync(h->sep_tiles.cnt, 0, sizeof(unsigned) * nTt, h->stream));
+    if ((st = tri_plan(h.get(), h->sep_tiles))) return st;
     CK(cudaStreamSynchronize(h->stream));
   }
   if ((st = h->alloc(d.u, m)) || (st = h->alloc(d.v, m)) || (st = h->alloc(d.t, m)) || (st = h->alloc(d.z, m)))

@@ -83,6 +83,9 @@ struct SolveDev {
 struct TriTiles {
   const double *tile; int32_t nT, n; double *part; unsigned *cnt;
   int32_t stream;               // tiles > 256 MB (HBM-streamed): evict-first loads
+  int32_t yc;                   // input blocks (tiles) per CTA
+  const int2 *work[2];          // yc > 1: per CTA of a pass (mode 0: L^{-1}, 1: L^{-T}): (X, first Y)
+  int32_t nwork[2];             // CTAs of a pass
 };
 
 // Horizon-partitioned separator solve (partition.cpp) on the device, this rank's pieces.
