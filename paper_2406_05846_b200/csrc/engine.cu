@@ -346,8 +346,7 @@ constexpr int kSepTile = 64;
 __global__ void __launch_bounds__(256) k_sep_tri(TriTiles d, int mode, const double *in, double *out,
                                                  const DevState *st, const double *ta = nullptr,
                                                  const double *tb = nullptr) {
-  pdl_enter();
-  if (st->done) return;
+  pdl_trigger();
   __shared__ double colp[8][kSepTile];
   __shared__ int last;
   const int b = blockIdx.x, nT = d.nT;
@@ -360,6 +359,8 @@ __global__ void __launch_bounds__(256) k_sep_tri(TriTiles d, int mode, const dou
   const double *Tt = d.tile + (int64_t)b * kSepTile * kSepTile;
   const int X = mode == 0 ? I : J;          // block this tile contributes to
   const int Y = mode == 0 ? J : I;          // block of the input it reads
+  // the tile (constant since setup) is loaded before the dependency wait: with programmatic
+  // dependent launch these loads overlap the previous kernel's tail
   double t0[8], t1[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) {             // rows warp*8 + k: 16 loads in flight per lane
@@ -367,6 +368,8 @@ __global__ void __launch_bounds__(256) k_sep_tri(TriTiles d, int mode, const dou
     t0[k] = ldf(Tt + r * kSepTile + lane, d.stream);
     t1[k] = ldf(Tt + r * kSepTile + lane + 32, d.stream);
   }
+  pdl_wait();
+  if (st->done) return;
   double *P = d.part + ((int64_t)X * nT + Y) * kSepTile;
   if (mode == 0) {
     const int j0 = J * kSepTile + lane, j1 = j0 + 32;
@@ -544,13 +547,6 @@ __global__ void __launch_bounds__(256) k_sep_tri_chunk(TriTiles d, int mode, con
     }
   }
   if (threadIdx.x == 0) d.cnt[X] = 0u;
-}
-
-// One separator pass: k_sep_tri (a tile per CTA) or, for chunked tiles, k_sep_tri_chunk.
-void sep_pass(const TriTiles &T, int mode, const double *in, double *out, const DevState *st, cudaStream_t s,
-              const double *ta = nullptr, const double *tb = nullptr) {
-  if (T.yc > 1) k_sep_tri_chunk<<<T.nwork[mode], 256, 0, s>>>(T, mode, in, out, st, ta, tb);
-  else k_sep_tri<<<T.nwork[mode], 256, 0, s>>>(T, mode, in, out, st, ta, tb);
 }
 
 // setup: lower 64x64 tiles of the lower-triangular matrix C (column-major nS x nS)
@@ -1083,11 +1079,21 @@ cudaError_t launch_k(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, si
 // 1 P1, 2 P2, 4 P6', 8 P7, 16 K-EIG, 32 update, 64 A X. Measured at pendulum N=30: all
 // edges +20 us (the early-resident CTAs of the GEMVs slow their predecessors); K-EIG
 // (its schedule table is built while P7 drains) and A X: 211 -> 207 us, repeatable.
-enum { kPdlP1 = 1, kPdlP2 = 2, kPdlP6b = 4, kPdlP7 = 8, kPdlEig = 16, kPdlUpd = 32, kPdlAx = 64 };
-constexpr int kPdlDefault = kPdlEig | kPdlAx;
+enum { kPdlP1 = 1, kPdlP2 = 2, kPdlP6b = 4, kPdlP7 = 8, kPdlEig = 16, kPdlUpd = 32, kPdlAx = 64, kPdlSep = 128 };
+constexpr int kPdlDefault = kPdlEig | kPdlAx;   // kPdlSep (128): +4% at pendulum N=30, opt-in
 bool use_pdl(const strom_admm *h, int edge) {
   static const int mask = [] { const char *e = getenv("STROM_PDL"); return e ? atoi(e) : kPdlDefault; }();
   return (mask & edge) && !h->prof_capture && h->xfer == 0;
+}
+
+// One separator pass: k_sep_tri (a tile per CTA) or, for chunked tiles, k_sep_tri_chunk.
+cudaError_t sep_pass(const TriTiles &T, int mode, const double *in, double *out, const DevState *st, cudaStream_t s,
+                     const double *ta = nullptr, const double *tb = nullptr, bool pdl = false) {
+  if (T.yc > 1) {
+    k_sep_tri_chunk<<<T.nwork[mode], 256, 0, s>>>(T, mode, in, out, st, ta, tb);
+    return cudaGetLastError();
+  }
+  return launch_k(pdl, k_sep_tri, T.nwork[mode], 256, 0, s, T, mode, in, out, st, ta, tb);
 }
 
 // Front half of one solve y = (eps I + AA*)^{-1} r (K-TRSV):
@@ -1125,11 +1131,11 @@ strom_status launch_solve_front(strom_admm *h, const RhsArgs &ra, double *y, int
     if (!h->part) {
       const TriTiles &T = h->sep_tiles;
       mark2(h, s2, "fork_trsv_p4_sep_LTinv");
-      sep_pass(T, 0, d.u + d.S0, d.z + d.S0, h->st, s2, dedup ? (const double *)h->p3tA : nullptr,
-               dedup ? (const double *)h->p3tB : nullptr); ++nl;
+      CK(sep_pass(T, 0, d.u + d.S0, d.z + d.S0, h->st, s2, dedup ? (const double *)h->p3tA : nullptr,
+                  dedup ? (const double *)h->p3tB : nullptr, use_pdl(h, kPdlSep))); ++nl;
       mark2_end(h, s2);
       mark2(h, s2, "fork_trsv_p5_sep_LTinvT");
-      sep_pass(T, 1, d.z + d.S0, y + d.S0, h->st, s2); ++nl;
+      CK(sep_pass(T, 1, d.z + d.S0, y + d.S0, h->st, s2, nullptr, nullptr, use_pdl(h, kPdlSep))); ++nl;
       mark2_end(h, s2);
     } else {
       const PartDev &p = h->pd;
