@@ -638,3 +638,46 @@ def test_batched_instances_match_separate_runs():
     assert ok and conv.all() and list(done) == its, (list(done), its)
     for g, h in zip(sep2, bat):
         assert np.array_equal(g.get()[0], h.get()[0])
+
+
+def test_kernel_work_table():
+    """strom_admm_kernel_work (the bench's roofline denominators): every marked
+    kernel of the instrumented iteration except the K-EIG classes has an entry, and the
+    A-based ones equal their closed form (12 B per stored nonzero + the vectors)."""
+    sdp = case("pend5")
+    g = make(sdp, check_every=5)
+    g.iterate(5)
+    names = {nm for nm, _ in g.kernel_times()}
+    assert names, "no instrumented iteration"
+    for nm in names:
+        w = g.kernel_work(nm)
+        if nm.startswith("eig_class"):
+            assert w is None
+        else:
+            assert w is not None and w[0] > 0 and w[1] >= 0, nm
+    nnz, n, m = sdp.nnz, sdp.n, sdp.m
+    assert g.kernel_work("spmv_AX_resid")[0] == 12.0 * nnz + 8.0 * (n + m)
+    assert g.kernel_work("update_X")[0] == 12.0 * nnz + 40.0 * n
+    assert g.kernel_work("no_such_kernel") is None
+
+
+def test_repeated_setup_reuses_pooled_memory():
+    """Handles take device memory from the stream-ordered pool (engine.cu pool_alloc) and give
+    it back on destruction: twelve setups of a pendulum N=30 handle in one process must not
+    grow the device footprint beyond a few handles' worth, and each result is unchanged."""
+    sdp = case("pend30")
+    ref = None
+    free0 = torch.cuda.mem_get_info()[0]
+    for k in range(12):
+        g = S.StromAdmm(S.StromSdp(sdp), S.strom_admm_default_config(check_every=5), stream=torch.cuda.Stream())
+        g.iterate(5)
+        X, _, _, _ = g.get()
+        if ref is None:
+            ref = X
+            per_handle = g.factor_info()["device_bytes"]
+        else:
+            assert np.array_equal(X, ref)
+        del g
+    torch.cuda.synchronize()
+    grown = free0 - torch.cuda.mem_get_info()[0]
+    assert grown <= 4 * per_handle + (64 << 20), (grown, per_handle)
