@@ -1,7 +1,3 @@
 mkdir -p gpurun_out/ab
-STROM_FACTOR_STREAM=1 timeout 900 python -m pytest tests -m gpu -q -x -p no:cacheprovider -k "solve_parity or 50_iter or final_obj or full_size" > gpurun_out/ab/pytest_chain_forced.log 2>&1
-timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/ab/pytest_chain.log 2>&1
-for c in landing50 flying60 carback30; do
-python tools/ab_time.py tools/ab/libB_chain.so,STROM_SEP_CHAIN=0 tools/ab/libB_chain.so $c 2 > gpurun_out/ab/chain_$c.txt 2>&1
-done
-python tools/ab_time.py tools/ab/libB_chain.so tools/ab/libB_chain.so,STROM_FACTOR_STREAM=1 30 2 > gpurun_out/ab/chain_pend30_forced.txt 2>&1
+L=paper_2406_05846_b200/libstrom.so
+python tools/ab_time.py $L,STROM_P3_DEDUP=0 $L 30 5 > gpurun_out/ab/p3d_pend30_5.txt 2>&1
