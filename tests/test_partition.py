@@ -43,7 +43,9 @@ def test_partitioned_solve_matches_factored_solve(name):
     r = o.apply_A(rng.standard_normal(sdp.n))       # r in range(A), as in Algorithm 1
     y_ref = o.solve(r)
     P = int(np.max(sdp.block_stage)) + 1
-    for R in (sorted({1, 2, 3, P}) if name != "pend8" else (P,)):
+    # R = 1 is the unpartitioned host solve (test_abi.py::test_host_factor_solve_matches_oracle);
+    # two ranks and one rank per stage bracket the partitions (each host_part call refactors)
+    for R in (sorted({2, P}) if name != "pend8" else (P,)):
         sends = [h.host_part(R, q, r) for q in range(R)]
         recv = np.sum(sends, axis=0)
         assert recv.size == (R - 1) * (70 if name.startswith("pend") else recv.size // max(R - 1, 1))
