@@ -1,2 +1,3 @@
 mkdir -p gpurun_out/micro
-./tools/micro/dmma > gpurun_out/micro/dmma.txt 2>&1
+./tools/micro/lat > gpurun_out/micro/lat.txt 2>&1
+./tools/micro/launch > gpurun_out/micro/launch.txt 2>&1
