@@ -589,6 +589,27 @@ def test_partition_path_with_nccl_allreduce_in_graph():
     assert sol[1] == "True" and sol[3] == "True", sol
 
 
+@pytest.mark.parametrize("env", [{"STROM_SEP_YC": "4", "STROM_FACTOR_STREAM": "1"},   # chunked separator, evict-first
+                                 {"STROM_P3_DEDUP": "0"},                              # row-per-warp P3
+                                 {"STROM_PDL": "255"}],                                # PDL on every edge
+                         ids=["sep-chunk-evict-first", "p3-rows", "pdl-all"])
+def test_non_default_paths_match_oracle(env):
+    """The run-time switches of DESIGN.md §9.3 select other kernels or launch modes (they are
+    read once per process, hence a subprocess): each must reproduce the oracle's 30 iterations
+    and reach the same tolerance."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", _FORCED % root], env=dict(os.environ, **env), capture_output=True,
+                         text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    err = [l for l in out.stdout.splitlines() if l.startswith("ERR")][0].split()
+    assert float(err[1]) <= 1e-9 and float(err[2]) <= 1e-9 and int(err[3]) == 30, err
+    sol = [l for l in out.stdout.splitlines() if l.startswith("SOLVE")][0].split()
+    assert sol[1] == "True" and sol[3] == "True", sol
+
+
 def test_compact_batch_matches_separate_runs():
     """A batch whose moment blocks outnumber the SMs (6 pendulum N=30 instances: 180
     order-55 blocks) captures 256-thread K-EIG CTAs, two per SM (strom_batch_create): the
